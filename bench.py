@@ -1,0 +1,386 @@
+#!/usr/bin/env python3
+"""Benchmark: particle pushes/s for the whole PIC step on B200 (sm_100a).
+
+Metric (BASELINE.json): particle pushes/sec/GPU for the whole step
+(advance_p + interpolators + scatter/unload + field solve + amortised sort)
+plus the % HBM roofline of advance_p.
+
+Default workload (BASELINE.json configs[1]): two-stream deck, 256^3 cells,
+64 ppc (two counter-drifting electron beams, 32 ppc each, drift +-0.2c,
+u_th 0.01), dt 0.25, h 1, blocked sort every 20 steps -> 1,073,741,824
+particles on one B200.  Synthetic data (device counter-based RNG load).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config two_stream|thermal|weak]
+  python bench.py --impl reference ...   # the reference CPU implementation
+
+Timed region: K whole steps (SimState::step + the reference run-loop's sort
+cadence, proj/src/sim.cpp:285-305) bracketed by CUDA events on the library's
+stream, synchronize on both sides, max over ranks.  Inputs (34 GB of particle
+records) are far larger than the 126 MB L2, so no flush is needed.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # configs[1]: two-stream / Weibel, 256^3, 64 ppc
+    "two_stream": dict(n=256, h=1.0, dt=0.25, sort_interval=20,
+                       species=[("beam_p", -1.0, 1.0, 32, 0.01, (0.2, 0.0, 0.0)),
+                                ("beam_m", -1.0, 1.0, 32, 0.01, (-0.2, 0.0, 0.0))]),
+    # configs[0]: uniform thermal e/i plasma, 64^3, 32 ppc each (bench_base.deck scaled)
+    "thermal": dict(n=64, h=1.0, dt=0.25, sort_interval=20,
+                    species=[("electron", -1.0, 1.0, 32, 0.1, (0.0, 0.0, 0.0)),
+                             ("ion", 1.0, 100.0, 32, 0.01, (0.0, 0.0, 0.0))]),
+    # configs[4]: weak scaling uniform plasma, ~1e9 particles per GPU
+    "weak": dict(n=256, h=1.0, dt=0.25, sort_interval=20,
+                 species=[("electron", -1.0, 1.0, 32, 0.1, (0.0, 0.0, 0.0)),
+                          ("ion", 1.0, 100.0, 32, 0.01, (0.0, 0.0, 0.0))]),
+}
+
+BYTES_PER_PUSH = 64  # 32 B record read + 32 B record written
+
+
+def deck_text(cfg, n=None, workers=1, seed=4):
+    """The reference deck (proj/src/deck.cpp grammar) for a config."""
+    n = n or cfg["n"]
+    L = n * cfg["h"]
+    lines = ["[grid]", f"nx = {n}", f"ny = {n}", f"nz = {n}", f"lx = {L}", f"ly = {L}", f"lz = {L}",
+             f"dt = {cfg['dt']}", "steps = 0"]
+    for name, q, m, ppc, uth, drift in cfg["species"]:
+        lines += [f"[species.{name}]", f"q = {q}", f"m = {m}", f"ppc = {ppc}", f"u_th = {uth}",
+                  f"drift = {drift[0]} {drift[1]} {drift[2]}", f"sort_interval = {cfg['sort_interval']}"]
+    lines += ["[run]", f"seed = {seed}", f"workers = {workers}"]
+    return "\n".join(lines) + "\n"
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k].lower() == "active"})
+        loaded = [s for s in sm if mx and s > 0.5 * max(mx)] or sm
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peak_gbs():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def profile_traffic():
+    """dram bytes per advance_p launch from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "advance_p_ncu.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return d.get("dram_bytes_per_push"), d
+    except Exception:
+        return None, None
+
+
+# ---------------------------------------------------------------------------
+def cpu_reference(cfg_name, steps, warmup, sample_n=64, workers=None):
+    """The reference CPU implementation (oracle/_ref: minipic compiled from its
+    sources, fp32, AVX2 lane) on a bounded sample of the workload: the same
+    deck physics on a sample_n^3 box, all host cores.  Returns pushes/s for
+    the whole step with the sort amortised over sort_interval."""
+    from oracle.bindings import Ref, ref_available
+
+    cfg = CONFIGS[cfg_name]
+    workers = workers or os.cpu_count() or 1
+    if not ref_available():
+        return None
+    ref = Ref()
+    n = min(sample_n, cfg["n"])
+    sim = ref.sim(deck_text(cfg, n=n, workers=workers))
+    npart = sum(sim.species(s)[1].size for s in range(sim.nspecies))
+    for _ in range(warmup):
+        sim.step(1)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        sim.step(1)
+        times.append(time.perf_counter() - t0)
+    # amortised sort: one blocked sort of every species (serial in the
+    # reference, particles.cpp:412-458), divided by sort_interval
+    t0 = time.perf_counter()
+    for s in range(sim.nspecies):
+        p, ids = sim.species(s)
+        ref.sort(p, ids, interleaved=False)
+    t_sort = time.perf_counter() - t0
+    t_step = statistics.median(times) + t_sort / cfg["sort_interval"]
+    return {
+        "value": npart / t_step, "unit": "particle pushes/s", "cores": workers, "kind": "reference",
+        "sample": f"{cfg_name} deck physics on {n}^3 cells ({npart} particles), median of {steps} steps "
+                  f"after {warmup} warm-up, + blocked sort/{cfg['sort_interval']}; minipic fp32 AVX2, "
+                  f"{workers} workers",
+        "step_s": statistics.median(times), "sort_s": t_sort,
+    }
+
+
+# ---------------------------------------------------------------------------
+def run_ours(args, rank, world):
+    import paper_2102_13133_b200 as pic
+
+    cfg = CONFIGS[args.config]
+    n = cfg["n"]
+    g = pic.make_grid(n, cfg["h"], dt=cfg["dt"])
+    ctx = pic.Context(g, device=args.device)
+    sids = []
+    for si, (name, q, m, ppc, uth, drift) in enumerate(cfg["species"]):
+        cap = ppc * g.interior
+        sid = ctx.add_species(name, q, m, cap)
+        ctx.load_synthetic(sid, ppc, uth, drift, seed=1234 + 7919 * rank)
+        sids.append(sid)
+    ctx.synchronize()
+    npart = sum(ctx.species_count(s) for s in sids)
+    sort_interval = cfg["sort_interval"]
+    step_count = [0]
+
+    def one_step():
+        ctx.step()
+        step_count[0] += 1
+        if sort_interval > 0 and step_count[0] % sort_interval == 0:
+            for s in sids:
+                ctx.sort_particles(s)
+
+    for _ in range(args.warmup):
+        one_step()
+    ctx.synchronize()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    # --- device-timed whole steps -------------------------------------------
+    clocks = ClockSampler(args.device)
+    clocks.start()
+    barrier()
+    ctx.synchronize()
+    l0 = ctx.launch_count()
+    ctx.event(0)
+    for _ in range(args.steps):
+        one_step()
+    ctx.event(1)
+    ctx.synchronize()
+    barrier()
+    ms = ctx.elapsed_ms(0, 1)
+    launches = ctx.launch_count() - l0
+    clk = clocks.stop()
+
+    # --- phase split (same steps again with PhaseTimings events) --------------
+    ctx.phase_timing(True)
+    ctx.phase_timings(reset=True)
+    nph = args.steps
+    for _ in range(nph):
+        one_step()
+    ctx.synchronize()
+    ph = ctx.phase_timings(reset=True)
+    ctx.phase_timing(False)
+    n_push_launch = nph * len(sids)
+    push_ms_per_launch = ph["push"] / n_push_launch
+    push_rate_kernel = npart * nph / (ph["push"] / 1e3)
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # --- e2e through the host-buffer C-ABI call --------------------------------
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(pic, ctx, sids, npart, args, world)
+    ctx.close()
+    return dict(ms=ms, npart=npart, launches=launches, clocks=clk, phases=ph, push_rate_kernel=push_rate_kernel,
+                push_ms_per_launch=push_ms_per_launch, nspecies=len(sids), grid=g, e2e=e2e)
+
+
+def run_e2e(pic, ctx, sids, npart, args, world):
+    """pic_step_host: every step uploads all species from pinned host
+    buffers, steps, and downloads them back (32 B/particle each way)."""
+    host = []
+    for s in sids:
+        p, ids = ctx.download_species(s)
+        pic.host_register(p)
+        pic.host_register(ids)
+        host.append((p, ids))
+    lanes = [h[0] for h in host]
+    idl = [h[1] for h in host]
+    ctx.step_host(lanes, idl)  # warm-up
+    ctx.synchronize()
+    k = max(1, args.e2e_steps)
+    t0 = time.perf_counter()
+    for _ in range(k):
+        ctx.step_host(lanes, idl)
+    dt = time.perf_counter() - t0
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([dt], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    for p, ids in host:
+        pic.host_unregister(p)
+        pic.host_unregister(ids)
+    b = sum(h[0].nbytes + h[1].nbytes for h in host)
+    return {"value": npart * k * world / dt, "unit": "particle pushes/s", "h2d_bytes_per_step": b,
+            "d2h_bytes_per_step": b, "steps": k, "ms_per_step": dt / k * 1e3}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=4)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="two_stream", choices=sorted(CONFIGS))
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-n", type=int, default=64)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    args.device = local
+    cfg = CONFIGS[args.config]
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        r = cpu_reference(args.config, max(1, min(args.steps, 3)), max(1, min(args.warmup, 1)),
+                          sample_n=args.cpu_sample_n)
+        if r is None:
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libminipic_ref.so not built"}))
+            return
+        line = {
+            "impl": "reference", "metric": "particle pushes/sec/GPU (advance_p, whole step)", "value": r["value"],
+            "unit": "particle pushes/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": r["step_s"] * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic (reference Rng load)",
+            "config": {"workload": args.config, "cells": f"{cfg['n']}^3", "sample": r["sample"]},
+            "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": r["value"], "unit": "particle pushes/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line))
+        return
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        dist.init_process_group("gloo")  # control plane only (barrier + max-reduce of timings)
+
+    res = run_ours(args, rank, world)
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+        return
+
+    ms_per_step = res["ms"] / args.steps
+    value = res["npart"] * world * args.steps / (res["ms"] / 1e3)
+    peak, peak_kind = measured_peak_gbs()
+    achieved = res["npart"] / res["nspecies"] * BYTES_PER_PUSH / (res["push_ms_per_launch"] / 1e3) / 1e9
+    traffic, prof = profile_traffic()
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            r = cpu_reference(args.config, 3, 1, sample_n=args.cpu_sample_n)
+            if r:
+                cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:  # the baseline is reported, not required
+            cpu = {"value": None, "error": str(e)[:200]}
+    g = res["grid"]
+    line = {
+        "metric": "particle pushes/sec/GPU (advance_p, whole step)",
+        "value": value,
+        "unit": "particle pushes/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (device counter-RNG load: uniform offsets, drifting Maxwellian momenta)",
+        "config": {"workload": args.config, "cells": f"{g.nx}x{g.ny}x{g.nz}", "particles_per_gpu": res["npart"],
+                   "ppc": sum(s[3] for s in cfg["species"]), "dt": g.dt, "sort_interval": cfg["sort_interval"],
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "inputs (34 GB of particle records) >> 126 MB L2; no flush",
+                   "push_kernel_rate": res["push_rate_kernel"],
+                   "phase_ms_per_step": {k: v / args.steps for k, v in res["phases"].items()}},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "kernel": "advance_p_kernel<false>",
+                     "bytes_per_push": BYTES_PER_PUSH, "peak_kind": peak_kind},
+        "cpu_baseline": cpu,
+        "e2e": res["e2e"],
+        "gpu_launches": res["launches"],
+        "clocks": res["clocks"],
+    }
+    print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,166 @@
+/*
+ * pic_b200.h — C-ABI drop-in boundary for the particle-in-cell hot path of
+ * arXiv 2102.13133 (VPIC 2.0; reference implementation "minipic",
+ * /root/reference/proj), re-implemented as hand-written sm_100a CUDA.
+ *
+ * Plain pointers, sizes and POD structs only; no C++ or torch types cross
+ * this boundary.  Every entry point returns a pic_status; the message of the
+ * most recent failure on the calling thread is pic_last_error().
+ *
+ * Array conventions match the reference's default storage
+ * (Layout::field_major, proj/include/minipic/layout.hpp:18-30), so a host
+ * that holds minipic buffers can hand their data() pointers straight in:
+ *   fields16 : 16 lanes x padded voxels, lane-major   (lanes.hpp:23-43)
+ *   interp18 : 18 lanes x padded voxels, lane-major   (lanes.hpp:48-69)
+ *   lanes7   :  7 lanes x n particles, lane-major     (lanes.hpp:8-19)
+ *   ids      :  n int32 voxel ids                     (types.hpp:20)
+ *   acc12    : padded voxels x 12 (record-major; the ScatterBuffer's dense
+ *              reduce() form, proj/src/layout.cpp:181-197)
+ * Device-side the data live in B200-native layouts; the
+ * upload / download calls convert.
+ *
+ * Error classes mirror proj/include/minipic/types.hpp:26-36 and
+ * proj/include/minipic/sim.hpp:66-69.  Device-detected failures (CFL
+ * violation, mover non-termination) are latched in a device flag and raised
+ * as PIC_RUN_ABORT at the next quiescence point (pic_synchronize, any
+ * download, pic_sim_step).
+ */
+#ifndef PIC_B200_H
+#define PIC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PIC_B200_ABI_VERSION 1
+
+typedef enum pic_status {
+  PIC_OK = 0,
+  PIC_USAGE_ERROR = 1,      /* minipic::usage_error      (types.hpp:27-30)  */
+  PIC_RUN_ABORT = 2,        /* minipic::run_abort        (types.hpp:33-36)  */
+  PIC_DECK_PARSE_ERROR = 3, /* minipic::deck_parse_error (sim.hpp:66-69)    */
+  PIC_CUDA_ERROR = 4,       /* CUDA runtime failure                          */
+  PIC_INTERNAL_ERROR = 5
+} pic_status;
+
+/* GridDescriptor (proj/include/minipic/grid.hpp:15-38), fp32. */
+typedef struct pic_grid {
+  int nx, ny, nz;
+  float hx, hy, hz, dt;
+} pic_grid;
+
+/* advance_p flags (proj/src/particles.cpp:255-262 exact_gyration / stage). */
+#define PIC_EXACT_GYRATION 0x1u
+#define PIC_DETERMINISTIC 0x2u /* DepositStage + replay_deposits order */
+
+/* sort orders (proj/include/minipic/particles.hpp:35) */
+#define PIC_SORT_BLOCKED 0
+#define PIC_SORT_INTERLEAVED 1
+
+typedef struct pic_context pic_context;
+
+int pic_version(void);
+const char* pic_last_error(void);
+
+/* ---- lifecycle ------------------------------------------------------------
+ * Replaces the device-side state SimState builds in its constructor
+ * (proj/src/sim.cpp:49-72): FieldArray, InterpolatorArray, ScatterBuffer.
+ * validate_grid (proj/src/grid.cpp:13-20) is applied. */
+int pic_context_create(int device, const pic_grid* grid, pic_context** out);
+int pic_context_destroy(pic_context* ctx);
+int pic_context_grid(pic_context* ctx, pic_grid* out);
+/* Quiescence point: waits for the context stream and raises latched device
+ * errors (proj/src/particles.cpp:190-194,240; proj/src/grid.cpp:42-43). */
+int pic_synchronize(pic_context* ctx);
+/* Pins (cudaHostRegister) / unpins a host range used for uploads/downloads. */
+int pic_host_register(void* ptr, size_t bytes);
+int pic_host_unregister(void* ptr);
+
+/* ---- species: Species / ParticleStore (proj/include/minipic/particles.hpp:18-45)
+ * capacity >= the largest count ever uploaded. */
+int pic_species_create(pic_context* ctx, const char* name, float q, float m,
+                       size_t capacity, int* out_species);
+int pic_species_count(pic_context* ctx, int species, size_t* out_n);
+/* copy_between host -> device mirror (proj/src/layout.cpp:99-118). */
+int pic_species_upload(pic_context* ctx, int species, size_t n,
+                       const float* lanes7, const int32_t* ids);
+int pic_species_download(pic_context* ctx, int species, float* lanes7,
+                         int32_t* ids);
+/* Native-record upload/download: two float4 streams per particle,
+ * pos = (dx, dy, dz, bits(id)) and mom = (ux, uy, uz, w) — the 32-byte
+ * device record, no layout conversion. */
+int pic_species_upload_records(pic_context* ctx, int species, size_t n,
+                               const void* pos16, const void* mom16);
+int pic_species_download_records(pic_context* ctx, int species, void* pos16,
+                                 void* mom16);
+/* Device-side synthetic load (counter-based RNG, NOT the reference's
+ * mt19937_64 stream): uniform offsets, drift + u_th * N(0,1) momenta, w = 1,
+ * ppc particles per interior voxel in voxel order (proj/src/sim.cpp:84-111
+ * shape).  For large benchmark decks; parity tests upload host-generated
+ * reference streams instead. */
+int pic_species_load_synthetic(pic_context* ctx, int species, int ppc,
+                               float u_th, const float drift[3],
+                               uint64_t seed);
+
+/* ---- fields: FieldArray (proj/include/minipic/fields.hpp:21-38) --------- */
+int pic_fields_upload(pic_context* ctx, const float* fields16);
+int pic_fields_download(pic_context* ctx, float* fields16);
+int pic_interpolators_download(pic_context* ctx, float* interp18);
+int pic_interpolators_upload(pic_context* ctx, const float* interp18);
+int pic_accumulator_download(pic_context* ctx, float* acc12);
+int pic_accumulator_upload(pic_context* ctx, const float* acc12);
+
+/* ---- the hot path ---------------------------------------------------------*/
+/* ScatterBuffer::clear (proj/src/layout.cpp:205-207). */
+int pic_clear_accumulator(pic_context* ctx);
+/* clear_currents (proj/src/fields.cpp:195-201). */
+int pic_clear_currents(pic_context* ctx);
+/* load_interpolators (proj/src/particles.cpp:42-111). */
+int pic_load_interpolators(pic_context* ctx);
+/* advance_particles (+ replay_deposits with PIC_DETERMINISTIC)
+ * (proj/src/particles.cpp:255-382): interpolator gather, Boris kick, face-
+ * splitting mover, charge-conserving deposit into the accumulator, periodic
+ * wrap of the final voxel. */
+int pic_advance_p(pic_context* ctx, int species, unsigned flags);
+/* ghost_fold_currents (proj/src/grid.cpp:78-99). */
+int pic_ghost_fold_currents(pic_context* ctx);
+/* unload_currents (proj/src/fields.cpp:208-251), jf += f_a * lane. */
+int pic_unload_currents(pic_context* ctx);
+/* advance_b (proj/src/fields.cpp:113-151) and advance_e (:153-193). */
+int pic_advance_b(pic_context* ctx, float frac);
+int pic_advance_e(pic_context* ctx);
+/* unload_currents fused with advance_e (identical results to calling
+ * pic_unload_currents then pic_advance_e). */
+int pic_unload_advance_e(pic_context* ctx);
+/* ghost_sync_fields (proj/src/fields.cpp:35-58). */
+int pic_ghost_sync_fields(pic_context* ctx);
+/* sort_particles (proj/src/particles.cpp:412-458). */
+int pic_sort_particles(pic_context* ctx, int species, int order);
+/* SimState::step (proj/src/sim.cpp:143-183) over every species of the
+ * context in creation order. */
+int pic_step(pic_context* ctx, unsigned flags);
+/* The same step with host-resident species (the reference's host
+ * advance_particles contract): uploads every species from lanes7[s]/ids[s],
+ * steps, downloads back into the same buffers. */
+int pic_step_host(pic_context* ctx, unsigned flags, float* const* lanes7,
+                  int32_t* const* ids);
+
+/* ---- timing: CUDA events on the context stream --------------------------*/
+int pic_event_record(pic_context* ctx, int slot); /* slot in [0, 64) */
+int pic_event_elapsed_ms(pic_context* ctx, int a, int b, float* ms);
+/* PhaseTimings (proj/include/minipic/sim.hpp:129-136) measured on the
+ * device with CUDA events: when enabled, pic_step / pic_sort_particles
+ * bracket their phases; pic_phase_timings returns cumulative milliseconds
+ * {interpolate, push, scatter, field, sort} (reset != 0 zeroes them). */
+int pic_phase_timing(pic_context* ctx, int enable);
+int pic_phase_timings(pic_context* ctx, double out_ms[5], int reset);
+/* Kernel launches issued by this context since creation. */
+int pic_launch_count(pic_context* ctx, uint64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PIC_B200_H */

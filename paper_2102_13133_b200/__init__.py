@@ -1,0 +1,326 @@
+"""paper_2102_13133_b200 — B200-native (sm_100a CUDA) particle-in-cell step.
+
+A from-scratch re-implementation of the hot path of arXiv 2102.13133 (VPIC
+2.0; reference implementation "minipic", /root/reference/proj) behind the C-ABI
+declared in ``include/pic_b200.h``.  This module is a thin ctypes binding over
+``libpic_b200.so``: every call goes to hand-written sm_100a kernels; there is
+no CPU fallback.  Importing on a machine without the built library raises.
+
+Array conventions are the reference's field-major ones (see pic_b200.h):
+fields ``(16, V)``, interpolators ``(18, V)``, particles ``(7, n)`` float32 +
+``(n,)`` int32 ids, accumulator ``(V, 12)``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libpic_b200.so")
+
+PIC_EXACT_GYRATION = 0x1
+PIC_DETERMINISTIC = 0x2
+SORT_BLOCKED = 0
+SORT_INTERLEAVED = 1
+
+# field lanes (proj/include/minipic/lanes.hpp:23-43)
+FIELD_LANES = ["ex", "ey", "ez", "div_e_err", "cbx", "cby", "cbz", "div_b_err",
+               "jfx", "jfy", "jfz", "rhof", "tcax", "tcay", "tcaz", "rhob"]
+F = {name: i for i, name in enumerate(FIELD_LANES)}
+
+
+class PicError(RuntimeError):
+    code = 5
+
+
+class UsageError(PicError):
+    """minipic::usage_error (proj/include/minipic/types.hpp:27-30)."""
+    code = 1
+
+
+class RunAbort(PicError):
+    """minipic::run_abort (proj/include/minipic/types.hpp:33-36)."""
+    code = 2
+
+
+class DeckParseError(PicError):
+    """minipic::deck_parse_error (proj/include/minipic/sim.hpp:66-69)."""
+    code = 3
+
+
+class CudaError(PicError):
+    code = 4
+
+
+_ERRS = {1: UsageError, 2: RunAbort, 3: DeckParseError, 4: CudaError}
+
+
+class Grid(C.Structure):
+    """pic_grid == GridDescriptor (proj/include/minipic/grid.hpp:15-38), fp32."""
+
+    _fields_ = [("nx", C.c_int), ("ny", C.c_int), ("nz", C.c_int),
+                ("hx", C.c_float), ("hy", C.c_float), ("hz", C.c_float), ("dt", C.c_float)]
+
+    @property
+    def padded(self) -> int:
+        return (self.nx + 2) * (self.ny + 2) * (self.nz + 2)
+
+    @property
+    def interior(self) -> int:
+        return self.nx * self.ny * self.nz
+
+    def voxel(self, ix, iy, iz):
+        return ix + (self.nx + 2) * (iy + (self.ny + 2) * iz)
+
+    def __repr__(self):
+        return (f"Grid(nx={self.nx}, ny={self.ny}, nz={self.nz}, hx={self.hx}, hy={self.hy}, "
+                f"hz={self.hz}, dt={self.dt})")
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Loads libpic_b200.so (fails loudly if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(LIB_PATH)
+    P = C.c_void_p
+    F32 = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
+    I32 = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
+    G = C.POINTER(Grid)
+    L.pic_last_error.restype = C.c_char_p
+    sigs = {
+        "pic_context_create": [C.c_int, G, C.POINTER(P)],
+        "pic_context_destroy": [P],
+        "pic_context_grid": [P, G],
+        "pic_synchronize": [P],
+        "pic_host_register": [P, C.c_size_t],
+        "pic_host_unregister": [P],
+        "pic_species_create": [P, C.c_char_p, C.c_float, C.c_float, C.c_size_t, C.POINTER(C.c_int)],
+        "pic_species_count": [P, C.c_int, C.POINTER(C.c_size_t)],
+        "pic_species_upload": [P, C.c_int, C.c_size_t, F32, I32],
+        "pic_species_download": [P, C.c_int, F32, I32],
+        "pic_species_upload_records": [P, C.c_int, C.c_size_t, P, P],
+        "pic_species_download_records": [P, C.c_int, P, P],
+        "pic_species_load_synthetic": [P, C.c_int, C.c_int, C.c_float, F32, C.c_uint64],
+        "pic_fields_upload": [P, F32],
+        "pic_fields_download": [P, F32],
+        "pic_interpolators_download": [P, F32],
+        "pic_interpolators_upload": [P, F32],
+        "pic_accumulator_download": [P, F32],
+        "pic_accumulator_upload": [P, F32],
+        "pic_clear_accumulator": [P],
+        "pic_clear_currents": [P],
+        "pic_load_interpolators": [P],
+        "pic_advance_p": [P, C.c_int, C.c_uint],
+        "pic_ghost_fold_currents": [P],
+        "pic_unload_currents": [P],
+        "pic_advance_b": [P, C.c_float],
+        "pic_advance_e": [P],
+        "pic_unload_advance_e": [P],
+        "pic_ghost_sync_fields": [P],
+        "pic_sort_particles": [P, C.c_int, C.c_int],
+        "pic_step": [P, C.c_uint],
+        "pic_step_host": [P, C.c_uint, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)],
+        "pic_event_record": [P, C.c_int],
+        "pic_event_elapsed_ms": [P, C.c_int, C.c_int, C.POINTER(C.c_float)],
+        "pic_launch_count": [P, C.POINTER(C.c_uint64)],
+        "pic_phase_timing": [P, C.c_int],
+        "pic_phase_timings": [P, C.POINTER(C.c_double), C.c_int],
+    }
+    for name, argtypes in sigs.items():
+        fn = getattr(L, name)
+        fn.argtypes = argtypes
+        fn.restype = C.c_int
+    _lib = L
+    return L
+
+
+def check(rc: int):
+    if rc:
+        msg = lib().pic_last_error().decode()
+        raise _ERRS.get(rc, PicError)(msg)
+
+
+def make_grid(n, h=1.0, dt=None, cfl_frac=0.5) -> Grid:
+    """Grid with dt = cfl_frac * cfl_limit (computed in fp32) unless given."""
+    nx, ny, nz = (n, n, n) if np.isscalar(n) else n
+    hx, hy, hz = (h, h, h) if np.isscalar(h) else h
+    if dt is None:
+        f32 = np.float32
+        s = f32(1) / (f32(hx) * f32(hx)) + f32(1) / (f32(hy) * f32(hy)) + f32(1) / (f32(hz) * f32(hz))
+        dt = f32(cfl_frac) * (f32(1) / np.sqrt(s, dtype=np.float32))
+    return Grid(int(nx), int(ny), int(nz), float(hx), float(hy), float(hz), float(np.float32(dt)))
+
+
+class Context:
+    """Device-resident PIC state on one GPU (pic_context)."""
+
+    def __init__(self, grid: Grid, device: int = 0):
+        self.grid = grid
+        self._h = C.c_void_p()
+        check(lib().pic_context_create(device, C.byref(grid), C.byref(self._h)))
+        self.species_names = []
+
+    def close(self):
+        if self._h:
+            check(lib().pic_context_destroy(self._h))
+            self._h = C.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def V(self) -> int:
+        return self.grid.padded
+
+    # --- species -----------------------------------------------------------
+    def add_species(self, name: str, q: float, m: float, capacity: int) -> int:
+        sid = C.c_int()
+        check(lib().pic_species_create(self._h, name.encode(), q, m, capacity, C.byref(sid)))
+        self.species_names.append(name)
+        return sid.value
+
+    def species_count(self, sid: int) -> int:
+        n = C.c_size_t()
+        check(lib().pic_species_count(self._h, sid, C.byref(n)))
+        return n.value
+
+    def upload_species(self, sid: int, lanes7: np.ndarray, ids: np.ndarray):
+        lanes7 = np.ascontiguousarray(lanes7, np.float32)
+        ids = np.ascontiguousarray(ids, np.int32)
+        assert lanes7.shape == (7, ids.size)
+        check(lib().pic_species_upload(self._h, sid, ids.size, lanes7, ids))
+
+    def download_species(self, sid: int):
+        n = self.species_count(sid)
+        p = np.zeros((7, n), np.float32)
+        ids = np.zeros(n, np.int32)
+        check(lib().pic_species_download(self._h, sid, p, ids))
+        return p, ids
+
+    def load_synthetic(self, sid: int, ppc: int, u_th: float, drift=(0.0, 0.0, 0.0), seed: int = 1):
+        check(lib().pic_species_load_synthetic(self._h, sid, ppc, u_th, np.asarray(drift, np.float32), seed))
+
+    # --- fields ------------------------------------------------------------
+    def upload_fields(self, f16: np.ndarray):
+        f16 = np.ascontiguousarray(f16, np.float32)
+        assert f16.shape == (16, self.V)
+        check(lib().pic_fields_upload(self._h, f16))
+
+    def download_fields(self) -> np.ndarray:
+        out = np.zeros((16, self.V), np.float32)
+        check(lib().pic_fields_download(self._h, out))
+        return out
+
+    def download_interpolators(self) -> np.ndarray:
+        out = np.zeros((18, self.V), np.float32)
+        check(lib().pic_interpolators_download(self._h, out))
+        return out
+
+    def upload_interpolators(self, i18: np.ndarray):
+        check(lib().pic_interpolators_upload(self._h, np.ascontiguousarray(i18, np.float32)))
+
+    def download_accumulator(self) -> np.ndarray:
+        out = np.zeros((self.V, 12), np.float32)
+        check(lib().pic_accumulator_download(self._h, out))
+        return out
+
+    def upload_accumulator(self, acc: np.ndarray):
+        check(lib().pic_accumulator_upload(self._h, np.ascontiguousarray(acc, np.float32)))
+
+    # --- hot path ------------------------------------------------------------
+    def clear_accumulator(self):
+        check(lib().pic_clear_accumulator(self._h))
+
+    def clear_currents(self):
+        check(lib().pic_clear_currents(self._h))
+
+    def load_interpolators(self):
+        check(lib().pic_load_interpolators(self._h))
+
+    def advance_p(self, sid: int, exact_gyration=False, deterministic=False):
+        flags = (PIC_EXACT_GYRATION if exact_gyration else 0) | (PIC_DETERMINISTIC if deterministic else 0)
+        check(lib().pic_advance_p(self._h, sid, flags))
+
+    def ghost_fold_currents(self):
+        check(lib().pic_ghost_fold_currents(self._h))
+
+    def unload_currents(self):
+        check(lib().pic_unload_currents(self._h))
+
+    def advance_b(self, frac: float):
+        check(lib().pic_advance_b(self._h, frac))
+
+    def advance_e(self):
+        check(lib().pic_advance_e(self._h))
+
+    def unload_advance_e(self):
+        check(lib().pic_unload_advance_e(self._h))
+
+    def ghost_sync_fields(self):
+        check(lib().pic_ghost_sync_fields(self._h))
+
+    def sort_particles(self, sid: int, order: int = SORT_BLOCKED):
+        check(lib().pic_sort_particles(self._h, sid, order))
+
+    def step(self, exact_gyration=False, deterministic=False):
+        flags = (PIC_EXACT_GYRATION if exact_gyration else 0) | (PIC_DETERMINISTIC if deterministic else 0)
+        check(lib().pic_step(self._h, flags))
+
+    def step_host(self, lanes7_list, ids_list, exact_gyration=False, deterministic=False):
+        """SimState::step with host-resident species buffers (copied in and out)."""
+        flags = (PIC_EXACT_GYRATION if exact_gyration else 0) | (PIC_DETERMINISTIC if deterministic else 0)
+        k = len(lanes7_list)
+        lp = (C.c_void_p * k)(*[a.ctypes.data for a in lanes7_list])
+        ip = (C.c_void_p * k)(*[a.ctypes.data for a in ids_list])
+        check(lib().pic_step_host(self._h, flags, lp, ip))
+
+    def synchronize(self):
+        check(lib().pic_synchronize(self._h))
+
+    # --- timing ----------------------------------------------------------------
+    def event(self, slot: int):
+        check(lib().pic_event_record(self._h, slot))
+
+    def elapsed_ms(self, a: int, b: int) -> float:
+        ms = C.c_float()
+        check(lib().pic_event_elapsed_ms(self._h, a, b, C.byref(ms)))
+        return ms.value
+
+    def phase_timing(self, enable: bool = True):
+        check(lib().pic_phase_timing(self._h, int(enable)))
+
+    def phase_timings(self, reset: bool = False) -> dict:
+        """Cumulative device ms per phase (PhaseTimings, sim.hpp:129-136)."""
+        out = (C.c_double * 5)()
+        check(lib().pic_phase_timings(self._h, out, int(reset)))
+        return dict(zip(("interpolate", "push", "scatter", "field", "sort"), list(out)))
+
+    def launch_count(self) -> int:
+        n = C.c_uint64()
+        check(lib().pic_launch_count(self._h, C.byref(n)))
+        return n.value
+
+
+def host_register(arr: np.ndarray):
+    check(lib().pic_host_register(arr.ctypes.data, arr.nbytes))
+
+
+def host_unregister(arr: np.ndarray):
+    check(lib().pic_host_unregister(arr.ctypes.data))

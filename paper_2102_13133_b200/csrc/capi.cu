@@ -1,0 +1,613 @@
+// Device context and the C-ABI (include/pic_b200.h).
+//
+// The context owns the device-resident state SimState builds in its
+// constructor (proj/src/sim.cpp:49-72) — fields, interpolators, the current
+// accumulator, the species stores — on one CUDA stream, plus a device error
+// latch that replaces the reference's immediate throws from inside the push
+// (proj/src/particles.cpp:190-194,240; proj/src/grid.cpp:42-43).
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <exception>
+#include <string>
+
+#include "pic_internal.hpp"
+
+namespace picb {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void* Context::scratch_bytes(int slot, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (scratch_size[slot] < bytes) {
+    if (scratch[slot]) {
+      CUDA_OK(cudaStreamSynchronize(stream));
+      CUDA_OK(cudaFree(scratch[slot]));
+      scratch[slot] = nullptr;
+      scratch_size[slot] = 0;
+    }
+    CUDA_OK(cudaMalloc(&scratch[slot], bytes));
+    scratch_size[slot] = bytes;
+  }
+  return scratch[slot];
+}
+
+void Context::phase_begin(int ph) {
+  if (!phase_timing) return;
+  if (ev_used + 2 > ev_pool.size()) {
+    for (int k = 0; k < 64; ++k) {
+      cudaEvent_t e;
+      CUDA_OK(cudaEventCreate(&e));
+      ev_pool.push_back(e);
+    }
+  }
+  CUDA_OK(cudaEventRecord(ev_pool[ev_used], stream));
+  ev_marks.emplace_back(ph, (int)ev_used);
+  ev_used += 2;
+  phase_open = ph;
+}
+
+void Context::phase_end() {
+  if (!phase_timing || phase_open < 0) return;
+  CUDA_OK(cudaEventRecord(ev_pool[(size_t)ev_marks.back().second + 1], stream));
+  phase_open = -1;
+  if (ev_used > 4096) resolve_phases();
+}
+
+void Context::resolve_phases() {
+  if (ev_marks.empty()) return;
+  CUDA_OK(cudaStreamSynchronize(stream));
+  for (const auto& m : ev_marks) {
+    float ms = 0;
+    CUDA_OK(cudaEventElapsedTime(&ms, ev_pool[(size_t)m.second], ev_pool[(size_t)m.second + 1]));
+    phase_ms[m.first] += ms;
+  }
+  ev_marks.clear();
+  ev_used = 0;
+}
+
+void Context::release() {
+  if (stream) cudaStreamSynchronize(stream);
+  for (auto& s : species) {
+    cudaFree(s.pos);
+    cudaFree(s.mom);
+    cudaFree(s.pos_alt);
+    cudaFree(s.mom_alt);
+  }
+  species.clear();
+  for (int i = 0; i < kScrN; ++i) {
+    cudaFree(scratch[i]);
+    scratch[i] = nullptr;
+  }
+  cudaFree(f);
+  cudaFree(interp);
+  cudaFree(acc);
+  cudaFree(d_err);
+  if (h_err) cudaFreeHost(h_err);
+  for (auto& e : events)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : ev_pool) cudaEventDestroy(e);
+  ev_pool.clear();
+  if (stream) cudaStreamDestroy(stream);
+  f = nullptr;
+  interp = nullptr;
+  acc = nullptr;
+  d_err = nullptr;
+  h_err = nullptr;
+  stream = nullptr;
+}
+
+// validate_grid / cfl_limit (proj/src/grid.cpp:7-20), in fp32.
+static void validate_grid(const pic_grid& g) {
+  if (g.nx < 2 || g.ny < 2 || g.nz < 2) throw UsageError("grid: interior counts must be >= 2");
+  if (!(g.hx > 0) || !(g.hy > 0) || !(g.hz > 0)) throw UsageError("grid: spacings must be positive");
+  const float s = 1.0f / (g.hx * g.hx) + 1.0f / (g.hy * g.hy) + 1.0f / (g.hz * g.hz);
+  const float cfl = 1.0f / std::sqrt(s);
+  if (!(g.dt > 0) || g.dt > 0.99f * cfl)
+    throw UsageError("grid: dt must satisfy 0 < dt <= 0.99 * cfl_limit");
+  const long long V = (long long)(g.nx + 2) * (g.ny + 2) * (g.nz + 2);
+  if (V >= (1LL << 31)) throw UsageError("grid: padded voxel count must fit int32 voxel ids");
+}
+
+Context* make_context(int device, const pic_grid& g) {
+  validate_grid(g);
+  auto* c = new Context();
+  try {
+    c->device = device;
+    c->grid = g;
+    GridC& gc = c->gc;
+    gc.nx = g.nx; gc.ny = g.ny; gc.nz = g.nz;
+    gc.pnx = g.nx + 2; gc.pny = g.ny + 2; gc.pnz = g.nz + 2;
+    gc.sy = gc.pnx;
+    gc.sz = gc.pnx * gc.pny;
+    gc.V = (long long)gc.pnx * gc.pny * gc.pnz;
+    gc.hx = g.hx; gc.hy = g.hy; gc.hz = g.hz; gc.dt = g.dt;
+    CUDA_OK(cudaSetDevice(device));
+    CUDA_OK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    const size_t V = (size_t)gc.V;
+    CUDA_OK(cudaMalloc(&c->f, F_COUNT * V * sizeof(float)));
+    CUDA_OK(cudaMalloc(&c->interp, kInterpF4 * V * sizeof(float4)));
+    CUDA_OK(cudaMalloc(&c->acc, 12 * V * sizeof(float)));
+    CUDA_OK(cudaMalloc(&c->d_err, sizeof(int)));
+    CUDA_OK(cudaMallocHost(&c->h_err, sizeof(int)));
+    CUDA_OK(cudaMemsetAsync(c->f, 0, F_COUNT * V * sizeof(float), c->stream));
+    CUDA_OK(cudaMemsetAsync(c->interp, 0, kInterpF4 * V * sizeof(float4), c->stream));
+    CUDA_OK(cudaMemsetAsync(c->acc, 0, 12 * V * sizeof(float), c->stream));
+    CUDA_OK(cudaMemsetAsync(c->d_err, 0, sizeof(int), c->stream));
+    CUDA_OK(cudaStreamSynchronize(c->stream));
+  } catch (...) {
+    c->release();
+    delete c;
+    throw;
+  }
+  return c;
+}
+
+void destroy_context(Context* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  c->release();
+  delete c;
+}
+
+void quiesce(Context& c) {
+  CUDA_OK(cudaMemcpyAsync(c.h_err, c.d_err, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+  CUDA_OK(cudaStreamSynchronize(c.stream));
+  const int e = *c.h_err;
+  if (e) {
+    CUDA_OK(cudaMemsetAsync(c.d_err, 0, sizeof(int), c.stream));
+    CUDA_OK(cudaStreamSynchronize(c.stream));
+    std::string msg;
+    if (e & kErrCfl) msg += "advance_particles: particle crossed more than one cell (CFL violation); ";
+    if (e & kErrMover) msg += "advance_particles: mover failed to terminate; ";
+    if (e & kErrWrap) msg += "wrap_periodic: displacement beyond one cell (CFL violation); ";
+    if (e & kErrVoxel) msg += "coords_of: voxel id out of range; ";
+    throw RunAbort(msg);
+  }
+}
+
+Species& species_at(Context& c, int sid) {
+  if (sid < 0 || sid >= (int)c.species.size()) throw UsageError("species index out of range");
+  return c.species[(size_t)sid];
+}
+
+// SimState::step (proj/src/sim.cpp:143-183).  unload_currents is fused into
+// advance_e: the first advance_b and ghost sync touch neither jf nor the
+// accumulator, so moving the unload past them changes no value.
+void step(Context& c, unsigned flags) {
+  const bool det = (flags & PIC_DETERMINISTIC) != 0;
+  const bool exact = (flags & PIC_EXACT_GYRATION) != 0;
+  // Phases as PhaseTimings: interpolate / push / scatter (clear + fold) /
+  // field (B, E with the fused unload, B, three ghost syncs).
+  c.phase_begin(Context::kPhScatter);
+  launch_clear_accumulator(c);  // scatter_->clear()
+  launch_clear_currents(c);     // clear_currents(fields_)
+  c.phase_end();
+  c.phase_begin(Context::kPhInterp);
+  launch_load_interpolators(c);
+  c.phase_end();
+  c.phase_begin(Context::kPhPush);
+  for (auto& s : c.species) {
+    if (det)
+      launch_advance_p_deterministic(c, s, exact);
+    else
+      launch_advance_p(c, s, exact);
+  }
+  c.phase_end();
+  c.phase_begin(Context::kPhScatter);
+  launch_ghost_fold(c);
+  c.phase_end();
+  c.phase_begin(Context::kPhField);
+  launch_advance_b(c, 0.5f);
+  launch_ghost_sync(c);
+  launch_unload_advance_e(c, true, true);
+  launch_ghost_sync(c);
+  launch_advance_b(c, 0.5f);
+  launch_ghost_sync(c);
+  c.phase_end();
+}
+
+}  // namespace picb
+
+// ===========================================================================
+// C-ABI
+using namespace picb;
+
+struct pic_context {
+  Context* c;
+};
+
+namespace {
+template <class Fn>
+int guard(Fn&& fn) {
+  try {
+    fn();
+    return PIC_OK;
+  } catch (const UsageError& e) {
+    g_last_error = e.what();
+    return PIC_USAGE_ERROR;
+  } catch (const RunAbort& e) {
+    g_last_error = e.what();
+    return PIC_RUN_ABORT;
+  } catch (const DeckParseError& e) {
+    g_last_error = e.what();
+    return PIC_DECK_PARSE_ERROR;
+  } catch (const CudaError& e) {
+    g_last_error = e.what();
+    return PIC_CUDA_ERROR;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return PIC_INTERNAL_ERROR;
+  }
+}
+Context& C_(pic_context* p) {
+  if (!p || !p->c) throw UsageError("null pic_context");
+  return *p->c;
+}
+void check_launch() {
+  CUDA_OK(cudaGetLastError());
+}
+}  // namespace
+
+extern "C" {
+
+int pic_version(void) { return PIC_B200_ABI_VERSION; }
+const char* pic_last_error(void) { return g_last_error.c_str(); }
+
+int pic_context_create(int device, const pic_grid* grid, pic_context** out) {
+  return guard([&] {
+    if (!grid || !out) throw UsageError("pic_context_create: null argument");
+    *out = nullptr;
+    Context* c = make_context(device, *grid);
+    *out = new pic_context{c};
+  });
+}
+
+int pic_context_destroy(pic_context* ctx) {
+  return guard([&] {
+    if (!ctx) return;
+    destroy_context(ctx->c);
+    delete ctx;
+  });
+}
+
+int pic_context_grid(pic_context* ctx, pic_grid* out) {
+  return guard([&] { *out = C_(ctx).grid; });
+}
+
+int pic_synchronize(pic_context* ctx) {
+  return guard([&] {
+    check_launch();
+    quiesce(C_(ctx));
+  });
+}
+
+int pic_host_register(void* ptr, size_t bytes) {
+  return guard([&] { CUDA_OK(cudaHostRegister(ptr, bytes, cudaHostRegisterDefault)); });
+}
+int pic_host_unregister(void* ptr) {
+  return guard([&] { CUDA_OK(cudaHostUnregister(ptr)); });
+}
+
+int pic_species_create(pic_context* ctx, const char* name, float q, float m, size_t capacity,
+                       int* out_species) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    if (!(m > 0)) throw UsageError("species: m must be positive");
+    Species s;
+    s.name = name ? name : "";
+    s.q = q;
+    s.m = m;
+    s.cap = capacity;
+    const size_t cap = capacity ? capacity : 1;
+    CUDA_OK(cudaMalloc(&s.pos, cap * sizeof(float4)));
+    CUDA_OK(cudaMalloc(&s.mom, cap * sizeof(float4)));
+    CUDA_OK(cudaMemsetAsync(s.pos, 0, cap * sizeof(float4), c.stream));
+    CUDA_OK(cudaMemsetAsync(s.mom, 0, cap * sizeof(float4), c.stream));
+    c.species.push_back(s);
+    *out_species = (int)c.species.size() - 1;
+  });
+}
+
+int pic_species_count(pic_context* ctx, int species, size_t* out_n) {
+  return guard([&] { *out_n = species_at(C_(ctx), species).n; });
+}
+
+static void validate_ids(const pic_grid& g, const int32_t* ids, size_t n) {
+  const int pnx = g.nx + 2, pny = g.ny + 2;
+  for (size_t i = 0; i < n; ++i) {
+    const int v = ids[i];
+    const int ix = v % pnx, rest = v / pnx, iy = rest % pny, iz = rest / pny;
+    if (v < 0 || ix < 1 || ix > g.nx || iy < 1 || iy > g.ny || iz < 1 || iz > g.nz)
+      throw UsageError("species upload: voxel id " + std::to_string(v) + " (particle " +
+                       std::to_string(i) + ") is not an interior voxel");
+  }
+}
+
+int pic_species_upload(pic_context* ctx, int species, size_t n, const float* lanes7,
+                       const int32_t* ids) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    Species& s = species_at(c, species);
+    if (n > s.cap) throw UsageError("species upload: count exceeds capacity");
+    validate_ids(c.grid, ids, n);
+    s.n = n;
+    if (n == 0) return;
+    char* stg = static_cast<char*>(c.scratch_bytes(Context::kScrStaging, n * 32));
+    float* d7 = reinterpret_cast<float*>(stg);
+    int32_t* did = reinterpret_cast<int32_t*>(stg + n * 28);
+    CUDA_OK(cudaMemcpyAsync(d7, lanes7, n * 28, cudaMemcpyHostToDevice, c.stream));
+    CUDA_OK(cudaMemcpyAsync(did, ids, n * 4, cudaMemcpyHostToDevice, c.stream));
+    launch_pack_species(c, s, d7, did, n);
+    check_launch();
+    CUDA_OK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int pic_species_download(pic_context* ctx, int species, float* lanes7, int32_t* ids) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    Species& s = species_at(c, species);
+    quiesce(c);
+    const size_t n = s.n;
+    if (n == 0) return;
+    char* stg = static_cast<char*>(c.scratch_bytes(Context::kScrStaging, n * 32));
+    float* d7 = reinterpret_cast<float*>(stg);
+    int32_t* did = reinterpret_cast<int32_t*>(stg + n * 28);
+    launch_unpack_species(c, s, d7, did);
+    check_launch();
+    CUDA_OK(cudaMemcpyAsync(lanes7, d7, n * 28, cudaMemcpyDeviceToHost, c.stream));
+    CUDA_OK(cudaMemcpyAsync(ids, did, n * 4, cudaMemcpyDeviceToHost, c.stream));
+    CUDA_OK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int pic_species_upload_records(pic_context* ctx, int species, size_t n, const void* pos16,
+                               const void* mom16) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    Species& s = species_at(c, species);
+    if (n > s.cap) throw UsageError("species upload: count exceeds capacity");
+    s.n = n;
+    if (n == 0) return;
+    CUDA_OK(cudaMemcpyAsync(s.pos, pos16, n * 16, cudaMemcpyHostToDevice, c.stream));
+    CUDA_OK(cudaMemcpyAsync(s.mom, mom16, n * 16, cudaMemcpyHostToDevice, c.stream));
+    CUDA_OK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int pic_species_download_records(pic_context* ctx, int species, void* pos16, void* mom16) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    Species& s = species_at(c, species);
+    quiesce(c);
+    if (s.n == 0) return;
+    CUDA_OK(cudaMemcpyAsync(pos16, s.pos, s.n * 16, cudaMemcpyDeviceToHost, c.stream));
+    CUDA_OK(cudaMemcpyAsync(mom16, s.mom, s.n * 16, cudaMemcpyDeviceToHost, c.stream));
+    CUDA_OK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int pic_species_load_synthetic(pic_context* ctx, int species, int ppc, float u_th,
+                               const float drift[3], uint64_t seed) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    if (ppc < 0) throw UsageError("load_synthetic: ppc must be >= 0");
+    const float zero[3] = {0, 0, 0};
+    launch_load_synthetic(c, species_at(c, species), ppc, u_th, drift ? drift : zero,
+                          seed + 0x9e3779b9ULL * (uint64_t)(species + 1));
+    check_launch();
+  });
+}
+
+int pic_fields_upload(pic_context* ctx, const float* fields16) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    CUDA_OK(cudaMemcpyAsync(c.f, fields16, F_COUNT * (size_t)c.gc.V * sizeof(float),
+                            cudaMemcpyHostToDevice, c.stream));
+    CUDA_OK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int pic_fields_download(pic_context* ctx, float* fields16) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    quiesce(c);
+    CUDA_OK(cudaMemcpyAsync(fields16, c.f, F_COUNT * (size_t)c.gc.V * sizeof(float),
+                            cudaMemcpyDeviceToHost, c.stream));
+    CUDA_OK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int pic_interpolators_download(pic_context* ctx, float* interp18) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    quiesce(c);
+    const size_t bytes = 18 * (size_t)c.gc.V * sizeof(float);
+    float* d = static_cast<float*>(c.scratch_bytes(Context::kScrStaging, bytes));
+    launch_interp_to_lanes(c, d);
+    check_launch();
+    CUDA_OK(cudaMemcpyAsync(interp18, d, bytes, cudaMemcpyDeviceToHost, c.stream));
+    CUDA_OK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int pic_interpolators_upload(pic_context* ctx, const float* interp18) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    const size_t bytes = 18 * (size_t)c.gc.V * sizeof(float);
+    float* d = static_cast<float*>(c.scratch_bytes(Context::kScrStaging, bytes));
+    CUDA_OK(cudaMemcpyAsync(d, interp18, bytes, cudaMemcpyHostToDevice, c.stream));
+    launch_lanes_to_interp(c, d);
+    check_launch();
+    CUDA_OK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int pic_accumulator_download(pic_context* ctx, float* acc12) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    quiesce(c);
+    CUDA_OK(cudaMemcpyAsync(acc12, c.acc, 12 * (size_t)c.gc.V * sizeof(float), cudaMemcpyDeviceToHost,
+                            c.stream));
+    CUDA_OK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int pic_accumulator_upload(pic_context* ctx, const float* acc12) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    CUDA_OK(cudaMemcpyAsync(c.acc, acc12, 12 * (size_t)c.gc.V * sizeof(float), cudaMemcpyHostToDevice,
+                            c.stream));
+    CUDA_OK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int pic_clear_accumulator(pic_context* ctx) {
+  return guard([&] { launch_clear_accumulator(C_(ctx)); });
+}
+int pic_clear_currents(pic_context* ctx) {
+  return guard([&] { launch_clear_currents(C_(ctx)); });
+}
+int pic_load_interpolators(pic_context* ctx) {
+  return guard([&] {
+    launch_load_interpolators(C_(ctx));
+    check_launch();
+  });
+}
+int pic_advance_p(pic_context* ctx, int species, unsigned flags) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    Species& s = species_at(c, species);
+    if (flags & PIC_DETERMINISTIC)
+      launch_advance_p_deterministic(c, s, (flags & PIC_EXACT_GYRATION) != 0);
+    else
+      launch_advance_p(c, s, (flags & PIC_EXACT_GYRATION) != 0);
+    check_launch();
+  });
+}
+int pic_ghost_fold_currents(pic_context* ctx) {
+  return guard([&] {
+    launch_ghost_fold(C_(ctx));
+    check_launch();
+  });
+}
+int pic_unload_currents(pic_context* ctx) {
+  return guard([&] {
+    launch_unload_advance_e(C_(ctx), true, false);
+    check_launch();
+  });
+}
+int pic_advance_b(pic_context* ctx, float frac) {
+  return guard([&] {
+    launch_advance_b(C_(ctx), frac);
+    check_launch();
+  });
+}
+int pic_advance_e(pic_context* ctx) {
+  return guard([&] {
+    launch_unload_advance_e(C_(ctx), false, true);
+    check_launch();
+  });
+}
+int pic_unload_advance_e(pic_context* ctx) {
+  return guard([&] {
+    launch_unload_advance_e(C_(ctx), true, true);
+    check_launch();
+  });
+}
+int pic_ghost_sync_fields(pic_context* ctx) {
+  return guard([&] {
+    launch_ghost_sync(C_(ctx));
+    check_launch();
+  });
+}
+int pic_sort_particles(pic_context* ctx, int species, int order) {
+  return guard([&] {
+    if (order != PIC_SORT_BLOCKED && order != PIC_SORT_INTERLEAVED) throw UsageError("sort: bad order");
+    Context& c = C_(ctx);
+    c.phase_begin(Context::kPhSort);
+    sort_species(c, species_at(c, species), order);
+    c.phase_end();
+    check_launch();
+  });
+}
+int pic_step(pic_context* ctx, unsigned flags) {
+  return guard([&] {
+    step(C_(ctx), flags);
+    check_launch();
+  });
+}
+
+int pic_step_host(pic_context* ctx, unsigned flags, float* const* lanes7, int32_t* const* ids) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    for (size_t s = 0; s < c.species.size(); ++s) {
+      Species& sp = c.species[s];
+      const size_t n = sp.n;
+      if (n == 0) continue;
+      char* stg = static_cast<char*>(c.scratch_bytes(Context::kScrStaging, n * 32));
+      CUDA_OK(cudaMemcpyAsync(stg, lanes7[s], n * 28, cudaMemcpyHostToDevice, c.stream));
+      CUDA_OK(cudaMemcpyAsync(stg + n * 28, ids[s], n * 4, cudaMemcpyHostToDevice, c.stream));
+      launch_pack_species(c, sp, reinterpret_cast<float*>(stg), reinterpret_cast<int32_t*>(stg + n * 28), n);
+    }
+    step(c, flags);
+    for (size_t s = 0; s < c.species.size(); ++s) {
+      Species& sp = c.species[s];
+      const size_t n = sp.n;
+      if (n == 0) continue;
+      char* stg = static_cast<char*>(c.scratch_bytes(Context::kScrStaging, n * 32));
+      launch_unpack_species(c, sp, reinterpret_cast<float*>(stg), reinterpret_cast<int32_t*>(stg + n * 28));
+      CUDA_OK(cudaMemcpyAsync(lanes7[s], stg, n * 28, cudaMemcpyDeviceToHost, c.stream));
+      CUDA_OK(cudaMemcpyAsync(ids[s], stg + n * 28, n * 4, cudaMemcpyDeviceToHost, c.stream));
+    }
+    check_launch();
+    quiesce(c);
+  });
+}
+
+int pic_event_record(pic_context* ctx, int slot) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    if (slot < 0 || slot >= 64) throw UsageError("event slot out of range");
+    if (!c.events[slot]) CUDA_OK(cudaEventCreate(&c.events[slot]));
+    CUDA_OK(cudaEventRecord(c.events[slot], c.stream));
+  });
+}
+
+int pic_event_elapsed_ms(pic_context* ctx, int a, int b, float* ms) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    if (a < 0 || a >= 64 || b < 0 || b >= 64 || !c.events[a] || !c.events[b])
+      throw UsageError("event slot not recorded");
+    CUDA_OK(cudaEventSynchronize(c.events[b]));
+    CUDA_OK(cudaEventElapsedTime(ms, c.events[a], c.events[b]));
+  });
+}
+
+int pic_phase_timing(pic_context* ctx, int enable) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    c.resolve_phases();
+    c.phase_timing = enable != 0;
+  });
+}
+
+int pic_phase_timings(pic_context* ctx, double out_ms[5], int reset) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    c.resolve_phases();
+    for (int k = 0; k < Context::kPhN; ++k) {
+      out_ms[k] = c.phase_ms[k];
+      if (reset) c.phase_ms[k] = 0;
+    }
+  });
+}
+
+int pic_launch_count(pic_context* ctx, uint64_t* out) {
+  return guard([&] { *out = C_(ctx).launches; });
+}
+
+}  // extern "C"

@@ -1,0 +1,438 @@
+// Field-side kernels for sm_100a: the per-voxel stencils of the step.
+//
+// Reference path restated (all /root/reference/proj):
+//   load_interpolators   src/particles.cpp:42-111
+//   advance_b            src/fields.cpp:113-151 (+ curl_line, src/kernels/scalar.cpp:36-41)
+//   advance_e            src/fields.cpp:153-193 (+ curl_line_j, scalar.cpp:43-49)
+//   unload_currents      src/fields.cpp:208-251
+//   ghost_sync_fields    src/fields.cpp:35-58
+//   ghost_fold_currents  src/grid.cpp:59-99
+//   clear_currents       src/fields.cpp:195-201
+//
+// Fields live lane-major (16 lanes x padded voxels, the reference's
+// field_major layout) so every stencil reads/writes unit-stride along x and
+// a warp's accesses coalesce.  All of these kernels are HBM-bound
+// streaming stencils; each does one pass with neighbours served from L1/L2.
+// unload_currents is restated in gather form: each interior edge sums its
+// <= 4 contributor voxels in ascending contributor index, which is exactly
+// the order the reference's z,y,x scatter loop adds them, so J is
+// bit-identical while no two threads write one edge.
+#include "pic_device.cuh"
+#include "pic_internal.hpp"
+
+namespace picb {
+
+namespace {
+
+struct Lanes {
+  float* p[F_COUNT];
+};
+
+__host__ Lanes lanes_of(Context& c) {
+  Lanes L;
+  for (int l = 0; l < F_COUNT; ++l) L.p[l] = c.f + (size_t)l * (size_t)c.gc.V;
+  return L;
+}
+
+__device__ __forceinline__ bool interior_coords(const GridC& g, long long idx, int& ix, int& iy,
+                                                int& iz) {
+  const long long nxy = (long long)g.nx * g.ny;
+  if (idx >= nxy * g.nz) return false;
+  iz = (int)(idx / nxy);
+  const int r = (int)(idx - (long long)iz * nxy);
+  iy = r / g.nx;
+  ix = r - iy * g.nx;
+  ++ix;
+  ++iy;
+  ++iz;
+  return true;
+}
+
+unsigned interior_blocks(const GridC& g, int threads) {
+  const long long n = (long long)g.nx * g.ny * g.nz;
+  return (unsigned)((n + threads - 1) / threads);
+}
+
+// ---- load_interpolators (particles.cpp:48-110) ----------------------------
+__global__ void __launch_bounds__(256)
+load_interpolators_kernel(GridC g, Lanes L, float4* __restrict__ out) {
+  int ix, iy, iz;
+  if (!interior_coords(g, (long long)blockIdx.x * blockDim.x + threadIdx.x, ix, iy, iz)) return;
+  const size_t v = (size_t)voxel_of(g, ix, iy, iz);
+  const size_t sx = 1, sy = (size_t)g.sy, sz = (size_t)g.sz;
+  const float* __restrict__ fex = L.p[F_EX];
+  const float* __restrict__ fey = L.p[F_EY];
+  const float* __restrict__ fez = L.p[F_EZ];
+  float w0, w1, w2, w3;
+  float4 r0, r1, r2, r3, r4;
+  w0 = fex[v]; w1 = fex[v + sy]; w2 = fex[v + sz]; w3 = fex[v + sy + sz];
+  r0.x = 0.25f * ((w3 + w0) + (w1 + w2));
+  r0.y = 0.25f * ((w3 - w0) + (w1 - w2));
+  r0.z = 0.25f * ((w3 - w0) - (w1 - w2));
+  r0.w = 0.25f * ((w3 + w0) - (w1 + w2));
+  w0 = fey[v]; w1 = fey[v + sz]; w2 = fey[v + sx]; w3 = fey[v + sz + sx];
+  r1.x = 0.25f * ((w3 + w0) + (w1 + w2));
+  r1.y = 0.25f * ((w3 - w0) + (w1 - w2));
+  r1.z = 0.25f * ((w3 - w0) - (w1 - w2));
+  r1.w = 0.25f * ((w3 + w0) - (w1 + w2));
+  w0 = fez[v]; w1 = fez[v + sx]; w2 = fez[v + sy]; w3 = fez[v + sx + sy];
+  r2.x = 0.25f * ((w3 + w0) + (w1 + w2));
+  r2.y = 0.25f * ((w3 - w0) + (w1 - w2));
+  r2.z = 0.25f * ((w3 - w0) - (w1 - w2));
+  r2.w = 0.25f * ((w3 + w0) - (w1 + w2));
+  w0 = L.p[F_BX][v]; w1 = L.p[F_BX][v + sx];
+  r3.x = 0.5f * (w1 + w0);
+  r3.y = 0.5f * (w1 - w0);
+  w0 = L.p[F_BY][v]; w1 = L.p[F_BY][v + sy];
+  r3.z = 0.5f * (w1 + w0);
+  r3.w = 0.5f * (w1 - w0);
+  w0 = L.p[F_BZ][v]; w1 = L.p[F_BZ][v + sz];
+  r4.x = 0.5f * (w1 + w0);
+  r4.y = 0.5f * (w1 - w0);
+  r4.z = 0.f;
+  r4.w = 0.f;
+  float4* o = out + v * kInterpF4;
+  o[0] = r0; o[1] = r1; o[2] = r2; o[3] = r3; o[4] = r4;
+}
+
+// ---- advance_b (fields.cpp:113-151) -----------------------------------------
+struct BCoef {
+  float c1x, c2x, c1y, c2y, c1z, c2z;
+};
+__global__ void __launch_bounds__(256)
+advance_b_kernel(GridC g, Lanes L, BCoef k) {
+  int ix, iy, iz;
+  if (!interior_coords(g, (long long)blockIdx.x * blockDim.x + threadIdx.x, ix, iy, iz)) return;
+  const size_t v = (size_t)voxel_of(g, ix, iy, iz);
+  const size_t sx = 1, sy = (size_t)g.sy, sz = (size_t)g.sz;
+  const float* __restrict__ ex = L.p[F_EX];
+  const float* __restrict__ ey = L.p[F_EY];
+  const float* __restrict__ ez = L.p[F_EZ];
+  const float exv = ex[v], eyv = ey[v], ezv = ez[v];
+  // dst = (dst + c1 * (p1 - p0)) + c2 * (q1 - q0)
+  L.p[F_BX][v] = (L.p[F_BX][v] + k.c1x * (ez[v + sy] - ezv)) + k.c2x * (ey[v + sz] - eyv);
+  L.p[F_BY][v] = (L.p[F_BY][v] + k.c1y * (ex[v + sz] - exv)) + k.c2y * (ez[v + sx] - ezv);
+  L.p[F_BZ][v] = (L.p[F_BZ][v] + k.c1z * (ey[v + sx] - eyv)) + k.c2z * (ex[v + sy] - exv);
+}
+
+// ---- unload_currents (gather form) + advance_e --------------------------------
+struct ECoef {
+  float c1x, c2x, c1y, c2y, c1z, c2z, c3;
+  float fx, fy, fz;  // unload scales h_a / (2 dt V) (fields.cpp:216-219)
+};
+
+// Adds f * val[o][i] onto jf in the order the reference's (z, y, x) voxel
+// loop visits the contributors: outer axis ascending, then inner axis
+// ascending.  o/i index 0 = the edge's own coordinate, 1 = the (wrapped)
+// minus-one neighbour; *_minus_first tells whether the neighbour's
+// coordinate is the smaller one (false only when wrapping at coordinate 1).
+__device__ __forceinline__ float gather4(float jf, float f, float v00, float v01, float v10,
+                                         float v11, bool outer_minus_first,
+                                         bool inner_minus_first) {
+  const float a0 = outer_minus_first ? (inner_minus_first ? v11 : v10) : (inner_minus_first ? v01 : v00);
+  const float a1 = outer_minus_first ? (inner_minus_first ? v10 : v11) : (inner_minus_first ? v00 : v01);
+  const float a2 = outer_minus_first ? (inner_minus_first ? v01 : v00) : (inner_minus_first ? v11 : v10);
+  const float a3 = outer_minus_first ? (inner_minus_first ? v00 : v01) : (inner_minus_first ? v10 : v11);
+  jf = jf + f * a0;
+  jf = jf + f * a1;
+  jf = jf + f * a2;
+  jf = jf + f * a3;
+  return jf;
+}
+
+template <bool kUnload, bool kAdvanceE>
+__global__ void __launch_bounds__(256)
+unload_advance_e_kernel(GridC g, Lanes L, const float* __restrict__ acc, ECoef k) {
+  int ix, iy, iz;
+  if (!interior_coords(g, (long long)blockIdx.x * blockDim.x + threadIdx.x, ix, iy, iz)) return;
+  const size_t v = (size_t)voxel_of(g, ix, iy, iz);
+  float jx = L.p[F_JX][v], jy = L.p[F_JY][v], jz = L.p[F_JZ][v];
+  if (kUnload) {
+    const int xm = ix == 1 ? g.nx : ix - 1;
+    const int ym = iy == 1 ? g.ny : iy - 1;
+    const int zm = iz == 1 ? g.nz : iz - 1;
+    const bool xmf = ix != 1, ymf = iy != 1, zmf = iz != 1;
+    const float* a_000 = acc + (size_t)v * 12;
+    const float* a_0y0 = acc + (size_t)voxel_of(g, ix, ym, iz) * 12;
+    const float* a_00z = acc + (size_t)voxel_of(g, ix, iy, zm) * 12;
+    const float* a_0yz = acc + (size_t)voxel_of(g, ix, ym, zm) * 12;
+    const float* a_x00 = acc + (size_t)voxel_of(g, xm, iy, iz) * 12;
+    const float* a_x0z = acc + (size_t)voxel_of(g, xm, iy, zm) * 12;
+    const float* a_xy0 = acc + (size_t)voxel_of(g, xm, ym, iz) * 12;
+    // jfx: outer z, inner y (jx0 own, jx1 y-minus, jx2 z-minus, jx3 both)
+    jx = gather4(jx, k.fx, a_000[0], a_0y0[1], a_00z[2], a_0yz[3], zmf, ymf);
+    // jfy: outer z, inner x (jy0 own, jy2 x-minus, jy1 z-minus, jy3 both)
+    jy = gather4(jy, k.fy, a_000[4], a_x00[6], a_00z[5], a_x0z[7], zmf, xmf);
+    // jfz: outer y, inner x (jz0 own, jz1 x-minus, jz2 y-minus, jz3 both)
+    jz = gather4(jz, k.fz, a_000[8], a_x00[9], a_0y0[10], a_xy0[11], ymf, xmf);
+    L.p[F_JX][v] = jx;
+    L.p[F_JY][v] = jy;
+    L.p[F_JZ][v] = jz;
+  }
+  if (kAdvanceE) {
+    const size_t sx = 1, sy = (size_t)g.sy, sz = (size_t)g.sz;
+    const float* __restrict__ bx = L.p[F_BX];
+    const float* __restrict__ by = L.p[F_BY];
+    const float* __restrict__ bz = L.p[F_BZ];
+    const float bxv = bx[v], byv = by[v], bzv = bz[v];
+    // dst = ((dst + c1 * (p1 - p0)) + c2 * (q1 - q0)) + c3 * r
+    L.p[F_EX][v] = ((L.p[F_EX][v] + k.c1x * (bzv - bz[v - sy])) + k.c2x * (byv - by[v - sz])) + k.c3 * jx;
+    L.p[F_EY][v] = ((L.p[F_EY][v] + k.c1y * (bxv - bx[v - sz])) + k.c2y * (bzv - bz[v - sx])) + k.c3 * jy;
+    L.p[F_EZ][v] = ((L.p[F_EZ][v] + k.c1z * (byv - by[v - sx])) + k.c2z * (bxv - bx[v - sy])) + k.c3 * jz;
+  }
+}
+
+// ---- ghost_sync_fields (fields.cpp:35-58) -----------------------------------
+// The reference's x -> y -> z plane copies leave every ghost voxel equal to
+// its fully wrapped interior image, so one pass over the six ghost faces
+// (edge/corner voxels written more than once with the same value) is
+// bit-identical.
+__device__ __forceinline__ int wrapc(int i, int n) { return i == 0 ? n : (i == n + 1 ? 1 : i); }
+
+__global__ void __launch_bounds__(256)
+ghost_sync_kernel(GridC g, Lanes L) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long fx = 2LL * g.pny * g.pnz, fy = 2LL * g.pnx * g.pnz, fz = 2LL * g.pnx * g.pny;
+  int ix, iy, iz;
+  if (t < fx) {
+    const int side = (int)(t & 1);
+    const long long r = t >> 1;
+    ix = side ? g.nx + 1 : 0;
+    iy = (int)(r % g.pny);
+    iz = (int)(r / g.pny);
+  } else if ((t -= fx) < fy) {
+    const int side = (int)(t & 1);
+    const long long r = t >> 1;
+    iy = side ? g.ny + 1 : 0;
+    ix = (int)(r % g.pnx);
+    iz = (int)(r / g.pnx);
+  } else if ((t -= fy) < fz) {
+    const int side = (int)(t & 1);
+    const long long r = t >> 1;
+    iz = side ? g.nz + 1 : 0;
+    ix = (int)(r % g.pnx);
+    iy = (int)(r / g.pnx);
+  } else {
+    return;
+  }
+  const size_t to = (size_t)voxel_of(g, ix, iy, iz);
+  const size_t from = (size_t)voxel_of(g, wrapc(ix, g.nx), wrapc(iy, g.ny), wrapc(iz, g.nz));
+  L.p[F_EX][to] = L.p[F_EX][from];
+  L.p[F_EY][to] = L.p[F_EY][from];
+  L.p[F_EZ][to] = L.p[F_EZ][from];
+  L.p[F_BX][to] = L.p[F_BX][from];
+  L.p[F_BY][to] = L.p[F_BY][from];
+  L.p[F_BZ][to] = L.p[F_BZ][from];
+}
+
+// ---- ghost_fold_currents (grid.cpp:59-99): three ordered passes ---------------
+__device__ __forceinline__ void fold_slot(float* acc, size_t from, size_t to) {
+  float4* a = reinterpret_cast<float4*>(acc);
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    float4 t = a[to * 3 + k];
+    const float4 s = a[from * 3 + k];
+    t.x = t.x + s.x; t.y = t.y + s.y; t.z = t.z + s.z; t.w = t.w + s.w;
+    a[to * 3 + k] = t;
+    a[from * 3 + k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+__global__ void fold_x_kernel(GridC g, float* acc) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)g.pny * g.pnz) return;
+  const int iy = (int)(t % g.pny), iz = (int)(t / g.pny);
+  fold_slot(acc, voxel_of(g, 0, iy, iz), voxel_of(g, g.nx, iy, iz));
+  fold_slot(acc, voxel_of(g, g.nx + 1, iy, iz), voxel_of(g, 1, iy, iz));
+}
+__global__ void fold_y_kernel(GridC g, float* acc) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)g.nx * g.pnz) return;
+  const int ix = (int)(t % g.nx) + 1, iz = (int)(t / g.nx);
+  fold_slot(acc, voxel_of(g, ix, 0, iz), voxel_of(g, ix, g.ny, iz));
+  fold_slot(acc, voxel_of(g, ix, g.ny + 1, iz), voxel_of(g, ix, 1, iz));
+}
+__global__ void fold_z_kernel(GridC g, float* acc) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)g.nx * g.ny) return;
+  const int ix = (int)(t % g.nx) + 1, iy = (int)(t / g.nx) + 1;
+  fold_slot(acc, voxel_of(g, ix, iy, 0), voxel_of(g, ix, iy, g.nz));
+  fold_slot(acc, voxel_of(g, ix, iy, g.nz + 1), voxel_of(g, ix, iy, 1));
+}
+
+// ---- layout conversion --------------------------------------------------------
+__global__ void pack_species_kernel(const float* __restrict__ l7, const int32_t* __restrict__ ids,
+                                    size_t n, float4* __restrict__ pos, float4* __restrict__ mom) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  pos[i] = make_float4(l7[i], l7[n + i], l7[2 * n + i], __int_as_float(ids[i]));
+  mom[i] = make_float4(l7[3 * n + i], l7[4 * n + i], l7[5 * n + i], l7[6 * n + i]);
+}
+__global__ void unpack_species_kernel(const float4* __restrict__ pos, const float4* __restrict__ mom,
+                                      size_t n, float* __restrict__ l7, int32_t* __restrict__ ids) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float4 p = pos[i], u = mom[i];
+  l7[i] = p.x; l7[n + i] = p.y; l7[2 * n + i] = p.z;
+  l7[3 * n + i] = u.x; l7[4 * n + i] = u.y; l7[5 * n + i] = u.z; l7[6 * n + i] = u.w;
+  ids[i] = __float_as_int(p.w);
+}
+__global__ void interp_to_lanes_kernel(const float4* __restrict__ c, size_t V, float* __restrict__ o) {
+  const size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  const float4* r = c + v * kInterpF4;
+  const float4 a = r[0], b = r[1], d = r[2], e = r[3], h = r[4];
+  const float vals[18] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, d.x, d.y, d.z, d.w,
+                          e.x, e.y, e.z, e.w, h.x, h.y};
+#pragma unroll
+  for (int l = 0; l < 18; ++l) o[(size_t)l * V + v] = vals[l];
+}
+__global__ void lanes_to_interp_kernel(const float* __restrict__ in, size_t V, float4* __restrict__ c) {
+  const size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  float x[20];
+#pragma unroll
+  for (int l = 0; l < 18; ++l) x[l] = in[(size_t)l * V + v];
+  x[18] = 0.f;
+  x[19] = 0.f;
+  float4* r = c + v * kInterpF4;
+#pragma unroll
+  for (int k = 0; k < 5; ++k) r[k] = make_float4(x[4 * k], x[4 * k + 1], x[4 * k + 2], x[4 * k + 3]);
+}
+
+// ---- synthetic load (benchmark decks): counter-based RNG ---------------------
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9e3779b97f4a7c15ULL;
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ float u01(uint64_t h) {  // [0, 1)
+  return (float)(h >> 40) * (1.0f / 16777216.0f);
+}
+__global__ void load_synthetic_kernel(GridC g, int ppc, float u_th, float dx0, float dy0, float dz0,
+                                      uint64_t seed, size_t n, float4* __restrict__ pos,
+                                      float4* __restrict__ mom) {
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const long long cell = (long long)(i / (size_t)ppc);
+  int ix, iy, iz;
+  interior_coords(g, cell, ix, iy, iz);
+  const uint64_t base = mix64(seed ^ (0x632be59bd9b4e019ULL * (uint64_t)(i + 1)));
+  const float x = 2.0f * u01(mix64(base + 1)) - 1.0f;
+  const float y = 2.0f * u01(mix64(base + 2)) - 1.0f;
+  const float z = 2.0f * u01(mix64(base + 3)) - 1.0f;
+  float nrm[4];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const float a = 1.0f - u01(mix64(base + 4 + 2 * k));  // (0, 1]
+    const float b = u01(mix64(base + 5 + 2 * k));
+    const float r = sqrtf(-2.0f * logf(a));
+    nrm[2 * k] = r * cospif(2.0f * b);
+    nrm[2 * k + 1] = r * sinpif(2.0f * b);
+  }
+  pos[i] = make_float4(x, y, z, __int_as_float(voxel_of(g, ix, iy, iz)));
+  mom[i] = make_float4(dx0 + u_th * nrm[0], dy0 + u_th * nrm[1], dz0 + u_th * nrm[2], 1.0f);
+}
+
+}  // namespace
+
+// ---- launchers -----------------------------------------------------------------
+void launch_load_interpolators(Context& c) {
+  load_interpolators_kernel<<<interior_blocks(c.gc, 256), 256, 0, c.stream>>>(c.gc, lanes_of(c), c.interp);
+  c.count_launch();
+}
+
+void launch_advance_b(Context& c, float frac) {
+  // constants computed on the host in real_t (fields.cpp:115-118, 133-138)
+  const float fdt = frac * c.grid.dt;
+  const float rhx = 1.0f / c.grid.hx, rhy = 1.0f / c.grid.hy, rhz = 1.0f / c.grid.hz;
+  BCoef k;
+  k.c1x = -fdt * rhy; k.c2x = fdt * rhz;
+  k.c1y = -fdt * rhz; k.c2y = fdt * rhx;
+  k.c1z = -fdt * rhx; k.c2z = fdt * rhy;
+  advance_b_kernel<<<interior_blocks(c.gc, 256), 256, 0, c.stream>>>(c.gc, lanes_of(c), k);
+  c.count_launch();
+}
+
+void launch_unload_advance_e(Context& c, bool unload, bool advance_e) {
+  const float dt = c.grid.dt;
+  const float rhx = 1.0f / c.grid.hx, rhy = 1.0f / c.grid.hy, rhz = 1.0f / c.grid.hz;
+  ECoef k;
+  k.c1x = dt * rhy; k.c2x = -dt * rhz;   // fields.cpp:175-180
+  k.c1y = dt * rhz; k.c2y = -dt * rhx;
+  k.c1z = dt * rhx; k.c2z = -dt * rhy;
+  k.c3 = -dt;
+  const float two_dt_v = 2.0f * dt * (c.grid.hx * c.grid.hy * c.grid.hz);  // fields.cpp:216-219
+  k.fx = c.grid.hx / two_dt_v;
+  k.fy = c.grid.hy / two_dt_v;
+  k.fz = c.grid.hz / two_dt_v;
+  const unsigned b = interior_blocks(c.gc, 256);
+  if (unload && advance_e)
+    unload_advance_e_kernel<true, true><<<b, 256, 0, c.stream>>>(c.gc, lanes_of(c), c.acc, k);
+  else if (unload)
+    unload_advance_e_kernel<true, false><<<b, 256, 0, c.stream>>>(c.gc, lanes_of(c), c.acc, k);
+  else if (advance_e)
+    unload_advance_e_kernel<false, true><<<b, 256, 0, c.stream>>>(c.gc, lanes_of(c), c.acc, k);
+  else
+    return;
+  c.count_launch();
+}
+
+void launch_ghost_sync(Context& c) {
+  const GridC& g = c.gc;
+  const long long n = 2LL * g.pny * g.pnz + 2LL * g.pnx * g.pnz + 2LL * g.pnx * g.pny;
+  ghost_sync_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(g, lanes_of(c));
+  c.count_launch();
+}
+
+void launch_ghost_fold(Context& c) {
+  const GridC& g = c.gc;
+  const long long nx = (long long)g.pny * g.pnz, ny = (long long)g.nx * g.pnz, nz = (long long)g.nx * g.ny;
+  fold_x_kernel<<<(unsigned)((nx + 255) / 256), 256, 0, c.stream>>>(g, c.acc);
+  fold_y_kernel<<<(unsigned)((ny + 255) / 256), 256, 0, c.stream>>>(g, c.acc);
+  fold_z_kernel<<<(unsigned)((nz + 255) / 256), 256, 0, c.stream>>>(g, c.acc);
+  c.count_launch(3);
+}
+
+void launch_clear_currents(Context& c) {
+  CUDA_OK(cudaMemsetAsync(c.f + (size_t)F_JX * c.gc.V, 0, 3 * (size_t)c.gc.V * sizeof(float), c.stream));
+}
+
+void launch_clear_accumulator(Context& c) {
+  CUDA_OK(cudaMemsetAsync(c.acc, 0, 12 * (size_t)c.gc.V * sizeof(float), c.stream));
+}
+
+void launch_pack_species(Context& c, Species& s, const float* l7, const int32_t* ids, size_t n) {
+  if (n == 0) return;
+  pack_species_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(l7, ids, n, s.pos, s.mom);
+  c.count_launch();
+}
+
+void launch_unpack_species(Context& c, Species& s, float* l7, int32_t* ids) {
+  if (s.n == 0) return;
+  unpack_species_kernel<<<(unsigned)((s.n + 255) / 256), 256, 0, c.stream>>>(s.pos, s.mom, s.n, l7, ids);
+  c.count_launch();
+}
+
+void launch_load_synthetic(Context& c, Species& s, int ppc, float u_th, const float drift[3],
+                           uint64_t seed) {
+  const size_t n = (size_t)ppc * (size_t)c.gc.nx * c.gc.ny * c.gc.nz;
+  if (n > s.cap) throw UsageError("load_synthetic: ppc * interior voxels exceeds species capacity");
+  s.n = n;
+  if (n == 0) return;
+  load_synthetic_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(
+      c.gc, ppc, u_th, drift[0], drift[1], drift[2], seed, n, s.pos, s.mom);
+  c.count_launch();
+}
+
+void launch_interp_to_lanes(Context& c, float* out18) {
+  interp_to_lanes_kernel<<<(unsigned)((c.gc.V + 255) / 256), 256, 0, c.stream>>>(c.interp, (size_t)c.gc.V, out18);
+  c.count_launch();
+}
+
+void launch_lanes_to_interp(Context& c, const float* in18) {
+  lanes_to_interp_kernel<<<(unsigned)((c.gc.V + 255) / 256), 256, 0, c.stream>>>(in18, (size_t)c.gc.V, c.interp);
+  c.count_launch();
+}
+
+}  // namespace picb

@@ -1,0 +1,130 @@
+// Host-side internal API of the sm_100a PIC library: the device-resident
+// context (the B200 replacement for SimState's FieldArray / InterpolatorArray
+// / ScatterBuffer / Species storage, proj/src/sim.cpp:49-72) and the kernel
+// launchers.  Not part of the public C-ABI (include/pic_b200.h).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/pic_b200.h"
+#include "pic_device.cuh"
+
+namespace picb {
+
+// Error classes of proj/include/minipic/types.hpp:26-36 / sim.hpp:66-69.
+struct UsageError : std::logic_error {
+  using std::logic_error::logic_error;
+};
+struct RunAbort : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct DeckParseError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define CUDA_OK(expr)                                                              \
+  do {                                                                             \
+    cudaError_t _e = (expr);                                                       \
+    if (_e != cudaSuccess)                                                         \
+      throw ::picb::CudaError(std::string(#expr) + ": " + cudaGetErrorString(_e)); \
+  } while (0)
+
+// Species / ParticleStore (proj/include/minipic/particles.hpp:18-45) with the
+// 32-byte device record split in two float4 streams.
+struct Species {
+  std::string name;
+  float q = 0, m = 1;
+  size_t n = 0, cap = 0;
+  float4* pos = nullptr;  // (dx, dy, dz, bits(id))
+  float4* mom = nullptr;  // (ux, uy, uz, w)
+  float4* pos_alt = nullptr;  // permutation target of the sort (lazy)
+  float4* mom_alt = nullptr;
+};
+
+struct Context {
+  int device = 0;
+  pic_grid grid{};
+  GridC gc{};
+  cudaStream_t stream = nullptr;
+  float* f = nullptr;         // 16 lanes x V, lane-major
+  float4* interp = nullptr;   // V x 5 float4
+  float* acc = nullptr;       // V x 12
+  int* d_err = nullptr;
+  int* h_err = nullptr;       // pinned
+  std::vector<Species> species;
+  uint64_t launches = 0;
+  cudaEvent_t events[64] = {};
+
+  enum ScratchSlot {
+    kScrStage = 0, kScrNseg, kScrOff, kScrSegKey, kScrSegW,
+    kScrKeyA, kScrValA, kScrKeyB, kScrValB, kScrHist, kScrScan,
+    kScrCount, kScrStart, kScrWithin, kScrStaging, kScrSmall, kScrN
+  };
+  void* scratch[kScrN] = {};
+  size_t scratch_size[kScrN] = {};
+
+  // PhaseTimings (proj/include/minipic/sim.hpp:129-136) on the device clock:
+  // CUDA events bracket each phase when enabled; resolved lazily.
+  enum Phase { kPhInterp = 0, kPhPush, kPhScatter, kPhField, kPhSort, kPhN };
+  bool phase_timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, int>> ev_marks;  // (phase, event index of phase start)
+  size_t ev_used = 0;
+  double phase_ms[kPhN] = {};
+  int phase_open = -1;
+  void phase_begin(int ph);
+  void phase_end();
+  void resolve_phases();
+
+  void count_launch(uint64_t k = 1) { launches += k; }
+  void* scratch_bytes(int slot, size_t bytes);
+  void release();
+};
+
+Context* make_context(int device, const pic_grid& g);
+void destroy_context(Context* c);
+// Waits for the stream, raises latched device errors as RunAbort.
+void quiesce(Context& c);
+Species& species_at(Context& c, int sid);
+
+// ---- launchers -------------------------------------------------------------
+void launch_advance_p(Context& c, Species& s, bool exact_gyration);
+void launch_advance_p_deterministic(Context& c, Species& s, bool exact_gyration);
+void launch_load_interpolators(Context& c);
+void launch_advance_b(Context& c, float frac);
+// unload (jf += f_a * lane, gather form) and/or advance_e in one pass.
+void launch_unload_advance_e(Context& c, bool unload, bool advance_e);
+void launch_ghost_sync(Context& c);
+void launch_ghost_fold(Context& c);
+void launch_clear_currents(Context& c);
+void launch_clear_accumulator(Context& c);
+void launch_pack_species(Context& c, Species& s, const float* lanes7_dev, const int32_t* ids_dev,
+                         size_t n);
+void launch_unpack_species(Context& c, Species& s, float* lanes7_dev, int32_t* ids_dev);
+void launch_load_synthetic(Context& c, Species& s, int ppc, float u_th, const float drift[3],
+                           uint64_t seed);
+void launch_interp_to_lanes(Context& c, float* out18);
+void launch_lanes_to_interp(Context& c, const float* in18);
+
+// ---- sort / scan primitives --------------------------------------------------
+int key_bits_for(long long max_key_exclusive);
+void exclusive_scan_u32(Context& c, const unsigned* in, unsigned* out, size_t n);
+// Stable LSD radix sort of (key, value) pairs on the context stream.  vals ==
+// nullptr means values are the identity 0..n-1.  Results are in
+// *keys_out / *vals_out (scratch buffers owned by the context).
+void radix_sort_pairs(Context& c, const unsigned* keys, const unsigned* vals, size_t n,
+                      int key_bits, unsigned** keys_out, unsigned** vals_out);
+void sort_species(Context& c, Species& s, int order);
+
+// ---- the step --------------------------------------------------------------
+void step(Context& c, unsigned flags);
+
+}  // namespace picb
