@@ -197,6 +197,10 @@ def run_ours(args, rank, world):
             for s in sids:
                 ctx.sort_particles(s)
 
+    # one sort of the freshly loaded (already voxel-ordered) stores allocates
+    # the sort scratch outside the timed region and leaves the order intact
+    for s in sids:
+        ctx.sort_particles(s)
     for _ in range(args.warmup):
         one_step()
     ctx.synchronize()

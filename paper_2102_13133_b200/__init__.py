@@ -312,6 +312,12 @@ class Context:
         check(lib().pic_phase_timings(self._h, out, int(reset)))
         return dict(zip(("interpolate", "push", "scatter", "field", "sort"), list(out)))
 
+    def _set_push_variant(self, variant: int):
+        """Benchmarking hook (not in the public C header): advance_p strategy."""
+        fn = lib().pic_internal_set_push_variant
+        fn.argtypes = [C.c_void_p, C.c_int]
+        check(fn(self._h, variant))
+
     def launch_count(self) -> int:
         n = C.c_uint64()
         check(lib().pic_launch_count(self._h, C.byref(n)))

@@ -124,8 +124,16 @@ Context* make_context(int device, const pic_grid& g) {
     gc.sz = gc.pnx * gc.pny;
     gc.V = (long long)gc.pnx * gc.pny * gc.pnz;
     gc.hx = g.hx; gc.hy = g.hy; gc.hz = g.hz; gc.dt = g.dt;
+    // m = ceil(2^64 / d) for d >= 2 (pnx, pny >= 4)
+    auto magic = [](unsigned d) {
+      const unsigned __int128 one = (unsigned __int128)1 << 64;
+      return (unsigned long long)((one + d - 1) / d);
+    };
+    gc.mag_pnx = magic((unsigned)gc.pnx);
+    gc.mag_pny = magic((unsigned)gc.pny);
     CUDA_OK(cudaSetDevice(device));
     CUDA_OK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CUDA_OK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     const size_t V = (size_t)gc.V;
     CUDA_OK(cudaMalloc(&c->f, F_COUNT * V * sizeof(float)));
     CUDA_OK(cudaMalloc(&c->interp, kInterpF4 * V * sizeof(float4)));
@@ -604,6 +612,11 @@ int pic_phase_timings(pic_context* ctx, double out_ms[5], int reset) {
       if (reset) c.phase_ms[k] = 0;
     }
   });
+}
+
+// Not in the public header: selects an advance_p strategy (benchmarking).
+int pic_internal_set_push_variant(pic_context* ctx, int variant) {
+  return guard([&] { C_(ctx).push_variant = variant; });
 }
 
 int pic_launch_count(pic_context* ctx, uint64_t* out) {

@@ -29,7 +29,14 @@ struct GridC {
   int sy, sz;          // +y / +z padded strides (stride_x == 1)
   long long V;         // padded voxels
   float hx, hy, hz, dt;
+  // exact division by pnx / pny: floor(v / d) == __umul64hi(v, m) with
+  // m = ceil(2^64 / d), valid for 0 <= v < 2^31 (host computes m).
+  unsigned long long mag_pnx, mag_pny;
 };
+
+__device__ __forceinline__ unsigned fast_div(unsigned v, unsigned long long m) {
+  return (unsigned)__umul64hi((unsigned long long)v, m);
+}
 
 // Interpolator record: 18 coefficients padded to 5 float4 (80 B), in the
 // reference lane order (lanes.hpp:48-69):
@@ -68,6 +75,39 @@ __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float 
   asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(addr), "f"(a),
                "f"(b), "f"(c), "f"(d)
                : "memory");
+}
+
+// ---- TMA bulk copies + mbarriers (sm_90+; the sm_100a TMA engine) ----------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+// global -> shared bulk copy completing on an mbarrier (bytes % 16 == 0)
+__device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gmem_src, unsigned bytes,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
 }
 
 }  // namespace picb

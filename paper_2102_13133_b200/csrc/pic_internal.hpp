@@ -61,6 +61,8 @@ struct Context {
   int* h_err = nullptr;       // pinned
   std::vector<Species> species;
   uint64_t launches = 0;
+  int push_variant = 0;   // advance_p strategy: 0 default, 1 TMA-staged, 2-4 ablations (push.cu)
+  int num_sms = 148;
   cudaEvent_t events[64] = {};
 
   enum ScratchSlot {

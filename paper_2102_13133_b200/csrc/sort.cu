@@ -204,23 +204,27 @@ int key_bits_for(long long max_key_exclusive) {
   return b;
 }
 
-void exclusive_scan_u32(Context& c, const unsigned* in, unsigned* out, size_t n) {
-  if (n == 0) return;
+static void scan_level(Context& c, const unsigned* in, unsigned* out, size_t n, unsigned* partial) {
   const size_t tiles = (n + kTile - 1) / kTile;
   if (tiles == 1) {
     scan_tile_kernel<<<1, kThreads, 0, c.stream>>>(in, n, nullptr, out);
     c.count_launch();
     return;
   }
-  // partial sums live in a fresh allocation per level (small)
-  unsigned* partial = nullptr;
-  CUDA_OK(cudaMallocAsync(&partial, tiles * sizeof(unsigned), c.stream));
   scan_reduce_kernel<<<(unsigned)tiles, kThreads, 0, c.stream>>>(in, n, partial);
   c.count_launch();
-  exclusive_scan_u32(c, partial, partial, tiles);
+  scan_level(c, partial, partial, tiles, partial + tiles);  // next level after this one
   scan_tile_kernel<<<(unsigned)tiles, kThreads, 0, c.stream>>>(in, n, partial, out);
   c.count_launch();
-  CUDA_OK(cudaFreeAsync(partial, c.stream));
+}
+
+void exclusive_scan_u32(Context& c, const unsigned* in, unsigned* out, size_t n) {
+  if (n == 0) return;
+  // partial sums of every level live back to back in one grow-only slot
+  size_t need = 0;
+  for (size_t t = (n + kTile - 1) / kTile; t > 1; t = (t + kTile - 1) / kTile) need += t;
+  unsigned* partial = static_cast<unsigned*>(c.scratch_bytes(Context::kScrScan, (need + 1) * sizeof(unsigned)));
+  scan_level(c, in, out, n, partial);
 }
 
 void radix_sort_pairs(Context& c, const unsigned* keys, const unsigned* vals, size_t n, int key_bits,

@@ -104,7 +104,7 @@ def test_fold_and_unload_bitwise(pic, orc, dims):
         assert_bitwise(ctx.download_fields(), want_f, "unload_advance_e")
 
 
-def _push_case(pic, orc, g, n, seed, q, m, u_scale, deterministic, exact=False):
+def _push_case(pic, orc, g, n, seed, q, m, u_scale, deterministic, exact=False, variant=None):
     rng = np.random.default_rng(seed)
     o = og(g)
     f = rand_fields(g, rng, scale=0.3, sync=lambda gg, ff: orc.ghost_sync(o, ff))
@@ -112,6 +112,8 @@ def _push_case(pic, orc, g, n, seed, q, m, u_scale, deterministic, exact=False):
     p, ids = rand_particles(g, rng, n, u_scale=u_scale)
     with pic.Context(g) as ctx:
         sid = ctx.add_species("s", q, m, n)
+        if variant is not None:
+            ctx._set_push_variant(variant)
         ctx.upload_species(sid, p, ids)
         ctx.upload_fields(f)
         ctx.load_interpolators()
@@ -140,6 +142,18 @@ def test_advance_p_parity(pic, orc, dims, n, u, deterministic):
         assert_close(gacc, wacc, ACC_RTOL, what="accumulator (fast)")
     # the case exercises the face-crossing tail and the periodic wrap
     assert (wids != _push_case.ids0).mean() > 0.02
+
+
+@pytest.mark.parametrize("variant", range(5))
+def test_advance_p_strategies(pic, orc, variant):
+    """Every advance_p deposit/tail strategy gives the bitwise particle state
+    and the accumulator within tolerance."""
+    g = pic.make_grid((10, 9, 8), 1.0, cfl_frac=0.9)
+    (gp, gids, gacc), (wp, wids, wacc) = _push_case(pic, orc, g, 60000, 13, -1.0, 1.0, 0.5, False,
+                                                    variant=variant)
+    assert_bitwise(gids, wids, "ids")
+    assert_bitwise(gp, wp, "particle lanes")
+    assert_close(gacc, wacc, ACC_RTOL, what="accumulator")
 
 
 def test_advance_p_unsorted_and_heavy_ions(pic, orc):
