@@ -318,6 +318,12 @@ class Context:
         fn.argtypes = [C.c_void_p, C.c_int]
         check(fn(self._h, variant))
 
+    def _set_host_chunk(self, particles: int):
+        """Testing hook (not in the public C header): pic_step_host chunk size."""
+        fn = lib().pic_internal_set_host_chunk
+        fn.argtypes = [C.c_void_p, C.c_size_t]
+        check(fn(self._h, particles))
+
     def launch_count(self) -> int:
         n = C.c_uint64()
         check(lib().pic_launch_count(self._h, C.byref(n)))

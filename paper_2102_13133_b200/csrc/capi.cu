@@ -5,6 +5,7 @@
 // accumulator, the species stores — on one CUDA stream, plus a device error
 // latch that replaces the reference's immediate throws from inside the push
 // (proj/src/particles.cpp:190-194,240; proj/src/grid.cpp:42-43).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -90,6 +91,19 @@ void Context::release() {
     if (e) cudaEventDestroy(e);
   for (auto& e : ev_pool) cudaEventDestroy(e);
   ev_pool.clear();
+  for (int b = 0; b < 2; ++b) {
+    if (ev_in[b]) cudaEventDestroy(ev_in[b]);
+    if (ev_packed[b]) cudaEventDestroy(ev_packed[b]);
+    if (ev_unpacked[b]) cudaEventDestroy(ev_unpacked[b]);
+    if (ev_out[b]) cudaEventDestroy(ev_out[b]);
+  }
+  for (auto& p : hstage) {
+    cudaFree(p);
+    p = nullptr;
+  }
+  if (cs_in) cudaStreamDestroy(cs_in);
+  if (cs_out) cudaStreamDestroy(cs_out);
+  cs_in = cs_out = nullptr;
   if (stream) cudaStreamDestroy(stream);
   f = nullptr;
   interp = nullptr;
@@ -184,11 +198,9 @@ Species& species_at(Context& c, int sid) {
 // SimState::step (proj/src/sim.cpp:143-183).  unload_currents is fused into
 // advance_e: the first advance_b and ghost sync touch neither jf nor the
 // accumulator, so moving the unload past them changes no value.
-void step(Context& c, unsigned flags) {
-  const bool det = (flags & PIC_DETERMINISTIC) != 0;
-  const bool exact = (flags & PIC_EXACT_GYRATION) != 0;
-  // Phases as PhaseTimings: interpolate / push / scatter (clear + fold) /
-  // field (B, E with the fused unload, B, three ghost syncs).
+// Phases as PhaseTimings: interpolate / push / scatter (clear + fold) /
+// field (B, E with the fused unload, B, three ghost syncs).
+static void step_prologue(Context& c) {
   c.phase_begin(Context::kPhScatter);
   launch_clear_accumulator(c);  // scatter_->clear()
   launch_clear_currents(c);     // clear_currents(fields_)
@@ -196,14 +208,9 @@ void step(Context& c, unsigned flags) {
   c.phase_begin(Context::kPhInterp);
   launch_load_interpolators(c);
   c.phase_end();
-  c.phase_begin(Context::kPhPush);
-  for (auto& s : c.species) {
-    if (det)
-      launch_advance_p_deterministic(c, s, exact);
-    else
-      launch_advance_p(c, s, exact);
-  }
-  c.phase_end();
+}
+
+static void step_epilogue(Context& c) {
   c.phase_begin(Context::kPhScatter);
   launch_ghost_fold(c);
   c.phase_end();
@@ -215,6 +222,94 @@ void step(Context& c, unsigned flags) {
   launch_advance_b(c, 0.5f);
   launch_ghost_sync(c);
   c.phase_end();
+}
+
+void step(Context& c, unsigned flags) {
+  const bool det = (flags & PIC_DETERMINISTIC) != 0;
+  const bool exact = (flags & PIC_EXACT_GYRATION) != 0;
+  step_prologue(c);
+  c.phase_begin(Context::kPhPush);
+  for (auto& s : c.species) {
+    if (det)
+      launch_advance_p_deterministic(c, s, exact);
+    else
+      launch_advance_p(c, s, exact);
+  }
+  c.phase_end();
+  step_epilogue(c);
+}
+
+// The step with host-resident species (pic_step_host).  The push of a
+// particle needs only the interpolators (built in the prologue) and writes
+// only its own record plus the accumulator, so species are streamed through
+// the device in chunks: H2D of chunk k+1, pack/push/unpack of chunk k and
+// D2H of chunk k-1 run concurrently on three streams with double-buffered
+// staging; the field epilogue follows the last push.  Host buffers should be
+// pinned (pic_host_register) for the copies to overlap.
+static void step_host(Context& c, unsigned flags, float* const* lanes7, int32_t* const* ids) {
+  const bool exact = (flags & PIC_EXACT_GYRATION) != 0;
+  size_t nmax = 0;
+  for (auto& s : c.species) nmax = std::max(nmax, s.n);
+  const size_t chunk = std::max<size_t>(1, std::min<size_t>(nmax, c.host_chunk));
+  if (!c.cs_in) {
+    CUDA_OK(cudaStreamCreateWithFlags(&c.cs_in, cudaStreamNonBlocking));
+    CUDA_OK(cudaStreamCreateWithFlags(&c.cs_out, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      CUDA_OK(cudaEventCreateWithFlags(&c.ev_in[b], cudaEventDisableTiming));
+      CUDA_OK(cudaEventCreateWithFlags(&c.ev_packed[b], cudaEventDisableTiming));
+      CUDA_OK(cudaEventCreateWithFlags(&c.ev_unpacked[b], cudaEventDisableTiming));
+      CUDA_OK(cudaEventCreateWithFlags(&c.ev_out[b], cudaEventDisableTiming));
+    }
+  }
+  if (c.hstage_bytes < chunk * 32) {
+    CUDA_OK(cudaStreamSynchronize(c.stream));
+    for (auto& p : c.hstage) {
+      cudaFree(p);
+      p = nullptr;
+    }
+    for (auto& p : c.hstage) CUDA_OK(cudaMalloc(&p, chunk * 32));
+    c.hstage_bytes = chunk * 32;
+  }
+  step_prologue(c);
+  c.phase_begin(Context::kPhPush);
+  size_t it = 0;
+  for (size_t si = 0; si < c.species.size(); ++si) {
+    Species& sp = c.species[si];
+    const size_t n = sp.n;
+    for (size_t start = 0; start < n; start += chunk, ++it) {
+      const size_t cnt = std::min(chunk, n - start);
+      const int b = (int)(it & 1);
+      char* in = static_cast<char*>(c.hstage[b]);
+      char* out = static_cast<char*>(c.hstage[2 + b]);
+      // H2D: 7 lane rows (host pitch n) + ids into in[b] once its last pack is done
+      CUDA_OK(cudaStreamWaitEvent(c.cs_in, c.ev_packed[b], 0));
+      CUDA_OK(cudaMemcpy2DAsync(in, cnt * 4, lanes7[si] + start, n * 4, cnt * 4, 7, cudaMemcpyHostToDevice,
+                                c.cs_in));
+      CUDA_OK(cudaMemcpyAsync(in + cnt * 28, ids[si] + start, cnt * 4, cudaMemcpyHostToDevice, c.cs_in));
+      CUDA_OK(cudaEventRecord(c.ev_in[b], c.cs_in));
+      // compute on the context stream
+      Species view = sp;
+      view.pos = sp.pos + start;
+      view.mom = sp.mom + start;
+      view.n = cnt;
+      CUDA_OK(cudaStreamWaitEvent(c.stream, c.ev_in[b], 0));
+      launch_pack_species(c, view, reinterpret_cast<float*>(in), reinterpret_cast<int32_t*>(in + cnt * 28), cnt);
+      CUDA_OK(cudaEventRecord(c.ev_packed[b], c.stream));
+      launch_advance_p(c, view, exact);
+      CUDA_OK(cudaStreamWaitEvent(c.stream, c.ev_out[b], 0));
+      launch_unpack_species(c, view, reinterpret_cast<float*>(out), reinterpret_cast<int32_t*>(out + cnt * 28));
+      CUDA_OK(cudaEventRecord(c.ev_unpacked[b], c.stream));
+      // D2H
+      CUDA_OK(cudaStreamWaitEvent(c.cs_out, c.ev_unpacked[b], 0));
+      CUDA_OK(cudaMemcpy2DAsync(lanes7[si] + start, n * 4, out, cnt * 4, cnt * 4, 7, cudaMemcpyDeviceToHost,
+                                c.cs_out));
+      CUDA_OK(cudaMemcpyAsync(ids[si] + start, out + cnt * 28, cnt * 4, cudaMemcpyDeviceToHost, c.cs_out));
+      CUDA_OK(cudaEventRecord(c.ev_out[b], c.cs_out));
+    }
+  }
+  c.phase_end();
+  step_epilogue(c);
+  CUDA_OK(cudaStreamSynchronize(c.cs_out));
 }
 
 }  // namespace picb
@@ -552,24 +647,29 @@ int pic_step(pic_context* ctx, unsigned flags) {
 int pic_step_host(pic_context* ctx, unsigned flags, float* const* lanes7, int32_t* const* ids) {
   return guard([&] {
     Context& c = C_(ctx);
-    for (size_t s = 0; s < c.species.size(); ++s) {
-      Species& sp = c.species[s];
-      const size_t n = sp.n;
-      if (n == 0) continue;
-      char* stg = static_cast<char*>(c.scratch_bytes(Context::kScrStaging, n * 32));
-      CUDA_OK(cudaMemcpyAsync(stg, lanes7[s], n * 28, cudaMemcpyHostToDevice, c.stream));
-      CUDA_OK(cudaMemcpyAsync(stg + n * 28, ids[s], n * 4, cudaMemcpyHostToDevice, c.stream));
-      launch_pack_species(c, sp, reinterpret_cast<float*>(stg), reinterpret_cast<int32_t*>(stg + n * 28), n);
-    }
-    step(c, flags);
-    for (size_t s = 0; s < c.species.size(); ++s) {
-      Species& sp = c.species[s];
-      const size_t n = sp.n;
-      if (n == 0) continue;
-      char* stg = static_cast<char*>(c.scratch_bytes(Context::kScrStaging, n * 32));
-      launch_unpack_species(c, sp, reinterpret_cast<float*>(stg), reinterpret_cast<int32_t*>(stg + n * 28));
-      CUDA_OK(cudaMemcpyAsync(lanes7[s], stg, n * 28, cudaMemcpyDeviceToHost, c.stream));
-      CUDA_OK(cudaMemcpyAsync(ids[s], stg + n * 28, n * 4, cudaMemcpyDeviceToHost, c.stream));
+    if (flags & PIC_DETERMINISTIC) {
+      // ordered replay needs whole-species passes: upload, step, download
+      for (size_t s = 0; s < c.species.size(); ++s) {
+        Species& sp = c.species[s];
+        const size_t n = sp.n;
+        if (n == 0) continue;
+        char* stg = static_cast<char*>(c.scratch_bytes(Context::kScrStaging, n * 32));
+        CUDA_OK(cudaMemcpyAsync(stg, lanes7[s], n * 28, cudaMemcpyHostToDevice, c.stream));
+        CUDA_OK(cudaMemcpyAsync(stg + n * 28, ids[s], n * 4, cudaMemcpyHostToDevice, c.stream));
+        launch_pack_species(c, sp, reinterpret_cast<float*>(stg), reinterpret_cast<int32_t*>(stg + n * 28), n);
+      }
+      step(c, flags);
+      for (size_t s = 0; s < c.species.size(); ++s) {
+        Species& sp = c.species[s];
+        const size_t n = sp.n;
+        if (n == 0) continue;
+        char* stg = static_cast<char*>(c.scratch_bytes(Context::kScrStaging, n * 32));
+        launch_unpack_species(c, sp, reinterpret_cast<float*>(stg), reinterpret_cast<int32_t*>(stg + n * 28));
+        CUDA_OK(cudaMemcpyAsync(lanes7[s], stg, n * 28, cudaMemcpyDeviceToHost, c.stream));
+        CUDA_OK(cudaMemcpyAsync(ids[s], stg + n * 28, n * 4, cudaMemcpyDeviceToHost, c.stream));
+      }
+    } else {
+      step_host(c, flags, lanes7, ids);
     }
     check_launch();
     quiesce(c);
@@ -617,6 +717,11 @@ int pic_phase_timings(pic_context* ctx, double out_ms[5], int reset) {
 // Not in the public header: selects an advance_p strategy (benchmarking).
 int pic_internal_set_push_variant(pic_context* ctx, int variant) {
   return guard([&] { C_(ctx).push_variant = variant; });
+}
+
+// Not in the public header: particles per chunk of the pic_step_host pipeline.
+int pic_internal_set_host_chunk(pic_context* ctx, size_t particles) {
+  return guard([&] { C_(ctx).host_chunk = particles ? particles : 1; });
 }
 
 int pic_launch_count(pic_context* ctx, uint64_t* out) {

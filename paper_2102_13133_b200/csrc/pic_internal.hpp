@@ -86,6 +86,14 @@ struct Context {
   void phase_end();
   void resolve_phases();
 
+  // host-buffer step pipeline (pic_step_host): copy-in / copy-out streams,
+  // double-buffered staging, ordering events
+  cudaStream_t cs_in = nullptr, cs_out = nullptr;
+  cudaEvent_t ev_in[2] = {}, ev_packed[2] = {}, ev_unpacked[2] = {}, ev_out[2] = {};
+  void* hstage[4] = {};  // in[0], in[1], out[0], out[1]
+  size_t hstage_bytes = 0;
+  size_t host_chunk = (size_t)1 << 25;  // particles per pipelined chunk
+
   void count_launch(uint64_t k = 1) { launches += k; }
   void* scratch_bytes(int slot, size_t bytes);
   void release();

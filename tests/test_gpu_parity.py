@@ -303,6 +303,33 @@ def test_step_host_matches_device_step(pic, orc):
         assert_bitwise(a.download_fields(), b.download_fields(), "step_host fields")
 
 
+@pytest.mark.parametrize("chunk", [997, 4096, 1 << 25])
+def test_step_host_pipeline_fast(pic, orc, chunk):
+    """The chunked 3-stream host-buffer step equals the device-resident step
+    (particle state bitwise: both see the same fields; fields within
+    tolerance: the atomic accumulation order differs)."""
+    g = pic.make_grid((10, 8, 6), 1.0, dt=0.25)
+    state = _deck_state(orc, g, [(-1.0, 1.0, 5, 0.15, (0.02, 0, 0)), (1.0, 50.0, 3, 0.02, (0, 0, 0))], seed=3)
+    with pic.Context(g) as a, pic.Context(g) as b:
+        b._set_host_chunk(chunk)
+        hosts = []
+        for q, m, p, ids in state:
+            sa = a.add_species("s", q, m, ids.size)
+            sb = b.add_species("s", q, m, ids.size)
+            a.upload_species(sa, p, ids)
+            b.upload_species(sb, p, ids)
+            hosts.append((p.copy(), ids.copy()))
+        a.step()
+        b.step_host([h[0] for h in hosts], [h[1] for h in hosts])
+        for sid, (hp, hid) in enumerate(hosts):
+            dp, did = a.download_species(sid)
+            assert_bitwise(hid, did, "ids")
+            assert_bitwise(hp, dp, "lanes")
+        fa, fb = a.download_fields(), b.download_fields()
+        for lane in (0, 1, 2, 4, 5, 6, 8, 9, 10):
+            assert_close(fb[lane], fa[lane], 1e-5, what=f"lane {lane}")
+
+
 def test_empty_species_and_zero_particles(pic):
     g = pic.make_grid((4, 4, 4))
     with pic.Context(g) as ctx:
