@@ -61,7 +61,9 @@ struct Context {
   int* h_err = nullptr;       // pinned
   std::vector<Species> species;
   uint64_t launches = 0;
-  int push_variant = 0;   // advance_p strategy: 0 default, 1 TMA-staged, 2-4 ablations (push.cu)
+  // advance_p strategy (push.cu): 7 = TMA-staged CTA rounds, 5 CTAs/SM (default);
+  // 0 = one particle per thread; 1, 5, 6, 8, 9 = TMA-staged ablations; 2-4 = other ablations
+  int push_variant = 7;
   int num_sms = 148;
   cudaEvent_t events[64] = {};
 

@@ -144,7 +144,7 @@ def test_advance_p_parity(pic, orc, dims, n, u, deterministic):
     assert (wids != _push_case.ids0).mean() > 0.02
 
 
-@pytest.mark.parametrize("variant", range(5))
+@pytest.mark.parametrize("variant", range(10))
 def test_advance_p_strategies(pic, orc, variant):
     """Every advance_p deposit/tail strategy gives the bitwise particle state
     and the accumulator within tolerance."""
