@@ -34,19 +34,29 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# Macro-particle charge and mass scale as 1/ppc (q/m fixed), so the plasma
+# frequency does not grow with the particle count: with the reference's w = 1
+# (proj/src/sim.cpp:106) a species of ppc particles per unit cell has
+# omega_p^2 = ppc q^2 / m.  An unscaled q = -1, m = 1 at 64 ppc would give
+# omega_p dt = 2 — the leapfrog stability limit — and the deck would heat
+# numerically instead of running the two-stream instability.
 CONFIGS = {
-    # configs[1]: two-stream / Weibel, 256^3, 64 ppc
+    # configs[1]: two-stream, 256^3, two counter-streaming electron beams of
+    # 32 ppc (64 ppc total) over a uniform neutralising background:
+    # omega_pe = 1, omega_pe dt = 0.25
     "two_stream": dict(n=256, h=1.0, dt=0.25, sort_interval=20,
-                       species=[("beam_p", -1.0, 1.0, 32, 0.01, (0.2, 0.0, 0.0)),
-                                ("beam_m", -1.0, 1.0, 32, 0.01, (-0.2, 0.0, 0.0))]),
-    # configs[0]: uniform thermal e/i plasma, 64^3, 32 ppc each (bench_base.deck scaled)
+                       species=[("beam_p", -1.0 / 64, 1.0 / 64, 32, 0.01, (0.2, 0.0, 0.0)),
+                                ("beam_m", -1.0 / 64, 1.0 / 64, 32, 0.01, (-0.2, 0.0, 0.0))]),
+    # configs[0]: uniform thermal e/i plasma, 64^3, 32 ppc each: bench_base.deck
+    # (proj/decks/bench_base.deck, 4 ppc, q = -1, m = 1) at 8x the particle count
+    # and the same plasma frequency (q, m scaled by 4/32)
     "thermal": dict(n=64, h=1.0, dt=0.25, sort_interval=20,
-                    species=[("electron", -1.0, 1.0, 32, 0.1, (0.0, 0.0, 0.0)),
-                             ("ion", 1.0, 100.0, 32, 0.01, (0.0, 0.0, 0.0))]),
+                    species=[("electron", -0.125, 0.125, 32, 0.1, (0.0, 0.0, 0.0)),
+                             ("ion", 0.125, 12.5, 32, 0.01, (0.0, 0.0, 0.0))]),
     # configs[4]: weak scaling uniform plasma, ~1e9 particles per GPU
     "weak": dict(n=256, h=1.0, dt=0.25, sort_interval=20,
-                 species=[("electron", -1.0, 1.0, 32, 0.1, (0.0, 0.0, 0.0)),
-                          ("ion", 1.0, 100.0, 32, 0.01, (0.0, 0.0, 0.0))]),
+                 species=[("electron", -0.125, 0.125, 32, 0.1, (0.0, 0.0, 0.0)),
+                          ("ion", 0.125, 12.5, 32, 0.01, (0.0, 0.0, 0.0))]),
 }
 
 BYTES_PER_PUSH = 64  # 32 B record read + 32 B record written
@@ -121,14 +131,15 @@ def measured_peak_gbs():
 
 
 def profile_traffic():
-    """dram bytes per advance_p launch from the committed ncu --set full summary."""
+    """DRAM bytes (read + write) per advance_p launch and per push from the
+    committed ncu --set full summary of the default kernel (profiles/)."""
     path = os.path.join(ROOT, "profiles", "advance_p_ncu.json")
     try:
         with open(path) as fh:
             d = json.load(fh)
-        return d.get("dram_bytes_per_push"), d
+        return d
     except Exception:
-        return None, None
+        return None
 
 
 # ---------------------------------------------------------------------------
@@ -343,7 +354,7 @@ def main():
     value = res["npart"] * world * args.steps / (res["ms"] / 1e3)
     peak, peak_kind = measured_peak_gbs()
     achieved = res["npart"] / res["nspecies"] * BYTES_PER_PUSH / (res["push_ms_per_launch"] / 1e3) / 1e9
-    traffic, prof = profile_traffic()
+    prof = profile_traffic()
     cpu = None
     if not args.no_cpu_baseline:
         try:
@@ -373,7 +384,12 @@ def main():
                    "push_kernel_rate": res["push_rate_kernel"],
                    "phase_ms_per_step": {k: v / args.steps for k, v in res["phases"].items()}},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": traffic, "kernel": "advance_p_kernel<false>",
+                     # measured DRAM bytes of one profiled launch (ncu, profiles/advance_p_ncu.json)
+                     "traffic": prof and prof.get("dram_bytes_per_launch"),
+                     "traffic_bytes_per_push": prof and prof.get("dram_bytes_per_push"),
+                     "traffic_launch_particles": prof and prof["launches"][0].get("particles"),
+                     "algorithmic_bytes_per_launch": res["npart"] / res["nspecies"] * BYTES_PER_PUSH,
+                     "kernel": prof and prof.get("kernel"),
                      "bytes_per_push": BYTES_PER_PUSH, "peak_kind": peak_kind},
         "cpu_baseline": cpu,
         "e2e": res["e2e"],

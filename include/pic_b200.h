@@ -148,6 +148,42 @@ int pic_step(pic_context* ctx, unsigned flags);
 int pic_step_host(pic_context* ctx, unsigned flags, float* const* lanes7,
                   int32_t* const* ids);
 
+/* ---- diagnostics -------------------------------------
+ * The diagnostic-cadence quantities of SimState::refresh_charge_diagnostics /
+ * current_diagnostics (proj/src/sim.cpp:230-266).  compute_div_errors and
+ * max_abs_lane are bit-exact; energies are summed in fp64 on the device and
+ * rho with float atomics (the reference reassociates these sums itself with
+ * its SIMD width / worker count), returned in fp32 like real_t. */
+/* clear_rho (proj/src/fields.cpp:203-206). */
+int pic_clear_rho(pic_context* ctx);
+/* deposit_rho (proj/src/particles.cpp:384-410). */
+int pic_deposit_rho(pic_context* ctx, int species);
+/* compute_div_errors (proj/src/fields.cpp:253-274). */
+int pic_compute_div_errors(pic_context* ctx);
+/* SimState::refresh_charge_diagnostics (proj/src/sim.cpp:230-234):
+ * clear_rho, deposit_rho of every species, compute_div_errors. */
+int pic_refresh_charge_diagnostics(pic_context* ctx);
+/* field_energy (proj/src/fields.cpp:276-299): e_b = {E energy, B energy}. */
+int pic_field_energy(pic_context* ctx, float e_b[2]);
+/* max_abs_lane (proj/src/fields.cpp:301-313), lane in [0, 16). */
+int pic_max_abs_lane(pic_context* ctx, int lane, float* out);
+/* kinetic_energy_centered (proj/src/particles.cpp:468-501) with the
+ * context's current interpolators when centered != 0, else kinetic_energy
+ * (proj/src/particles.cpp:460-466). */
+int pic_kinetic_energy(pic_context* ctx, int species, int centered, float* out);
+/* DiagnosticsRecord (proj/include/minipic/sim.hpp:88-100) minus the wall
+ * clock fields; kinetic[] receives one entry per species (kinetic_cap >=
+ * species count). */
+typedef struct pic_diag {
+  float e_energy, b_energy, total_energy, max_div_e_err, max_div_b_err;
+  uint64_t particle_count;
+} pic_diag;
+/* SimState::current_diagnostics (proj/src/sim.cpp:236-266): field energy,
+ * load_interpolators, centred kinetic energy per species, total, max div
+ * errors, particle count.  Call pic_refresh_charge_diagnostics first for
+ * current div errors, as SimState::run does on the diag cadence. */
+int pic_diagnostics(pic_context* ctx, pic_diag* out, float* kinetic, size_t kinetic_cap);
+
 /* ---- timing: CUDA events on the context stream --------------------------*/
 int pic_event_record(pic_context* ctx, int slot); /* slot in [0, 64) */
 int pic_event_elapsed_ms(pic_context* ctx, int a, int b, float* ms);

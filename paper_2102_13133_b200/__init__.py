@@ -79,6 +79,13 @@ class Grid(C.Structure):
                 f"hz={self.hz}, dt={self.dt})")
 
 
+class Diag(C.Structure):
+    """pic_diag == DiagnosticsRecord (proj/include/minipic/sim.hpp:88-100) minus wall clock."""
+
+    _fields_ = [("e_energy", C.c_float), ("b_energy", C.c_float), ("total_energy", C.c_float),
+                ("max_div_e_err", C.c_float), ("max_div_b_err", C.c_float), ("particle_count", C.c_uint64)]
+
+
 _lib = None
 
 
@@ -133,6 +140,14 @@ def lib() -> C.CDLL:
         "pic_launch_count": [P, C.POINTER(C.c_uint64)],
         "pic_phase_timing": [P, C.c_int],
         "pic_phase_timings": [P, C.POINTER(C.c_double), C.c_int],
+        "pic_clear_rho": [P],
+        "pic_deposit_rho": [P, C.c_int],
+        "pic_compute_div_errors": [P],
+        "pic_refresh_charge_diagnostics": [P],
+        "pic_field_energy": [P, C.POINTER(C.c_float)],
+        "pic_max_abs_lane": [P, C.c_int, C.POINTER(C.c_float)],
+        "pic_kinetic_energy": [P, C.c_int, C.c_int, C.POINTER(C.c_float)],
+        "pic_diagnostics": [P, C.POINTER(Diag), C.POINTER(C.c_float), C.c_size_t],
     }
     for name, argtypes in sigs.items():
         fn = getattr(L, name)
@@ -293,6 +308,45 @@ class Context:
 
     def synchronize(self):
         check(lib().pic_synchronize(self._h))
+
+    # --- diagnostics (proj/src/sim.cpp:230-266) ---------------------------------
+    def clear_rho(self):
+        check(lib().pic_clear_rho(self._h))
+
+    def deposit_rho(self, sid: int):
+        check(lib().pic_deposit_rho(self._h, sid))
+
+    def compute_div_errors(self):
+        check(lib().pic_compute_div_errors(self._h))
+
+    def refresh_charge_diagnostics(self):
+        check(lib().pic_refresh_charge_diagnostics(self._h))
+
+    def field_energy(self):
+        out = (C.c_float * 2)()
+        check(lib().pic_field_energy(self._h, out))
+        return float(out[0]), float(out[1])
+
+    def max_abs_lane(self, lane: int) -> float:
+        out = C.c_float()
+        check(lib().pic_max_abs_lane(self._h, lane, C.byref(out)))
+        return out.value
+
+    def kinetic_energy(self, sid: int, centered: bool = True) -> float:
+        out = C.c_float()
+        check(lib().pic_kinetic_energy(self._h, sid, int(centered), C.byref(out)))
+        return out.value
+
+    def diagnostics(self) -> dict:
+        """SimState::current_diagnostics (sim.cpp:236-266) on the device."""
+        d = Diag()
+        k = max(1, len(self.species_names))
+        kin = (C.c_float * k)()
+        check(lib().pic_diagnostics(self._h, C.byref(d), kin, k))
+        return {"e_energy": d.e_energy, "b_energy": d.b_energy,
+                "kinetic": [kin[i] for i in range(len(self.species_names))],
+                "total_energy": d.total_energy, "max_div_e_err": d.max_div_e_err,
+                "max_div_b_err": d.max_div_b_err, "particle_count": int(d.particle_count)}
 
     # --- timing ----------------------------------------------------------------
     def event(self, slot: int):

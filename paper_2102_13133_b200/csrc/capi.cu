@@ -678,6 +678,81 @@ int pic_step_host(pic_context* ctx, unsigned flags, float* const* lanes7, int32_
   });
 }
 
+int pic_clear_rho(pic_context* ctx) {
+  return guard([&] { launch_clear_rho(C_(ctx)); });
+}
+int pic_deposit_rho(pic_context* ctx, int species) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    launch_deposit_rho(c, species_at(c, species));
+    check_launch();
+  });
+}
+int pic_compute_div_errors(pic_context* ctx) {
+  return guard([&] {
+    launch_compute_div_errors(C_(ctx));
+    check_launch();
+  });
+}
+int pic_refresh_charge_diagnostics(pic_context* ctx) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    launch_clear_rho(c);
+    for (auto& s : c.species) launch_deposit_rho(c, s);
+    launch_compute_div_errors(c);
+    check_launch();
+  });
+}
+int pic_field_energy(pic_context* ctx, float e_b[2]) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    quiesce(c);
+    field_energy(c, e_b);
+  });
+}
+int pic_max_abs_lane(pic_context* ctx, int lane, float* out) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    if (lane < 0 || lane >= F_COUNT) throw UsageError("max_abs_lane: lane out of range");
+    quiesce(c);
+    *out = max_abs_lane(c, lane);
+  });
+}
+int pic_kinetic_energy(pic_context* ctx, int species, int centered, float* out) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    Species& s = species_at(c, species);
+    quiesce(c);
+    *out = kinetic_energy(c, s, centered != 0);
+  });
+}
+int pic_diagnostics(pic_context* ctx, pic_diag* out, float* kinetic, size_t kinetic_cap) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    if (!out) throw UsageError("diagnostics: null output");
+    if (kinetic_cap < c.species.size() || (!kinetic && !c.species.empty()))
+      throw UsageError("diagnostics: kinetic[] smaller than the species count");
+    quiesce(c);
+    float eb[2];
+    field_energy(c, eb);
+    out->e_energy = eb[0];
+    out->b_energy = eb[1];
+    float total = eb[0] + eb[1];
+    launch_load_interpolators(c);  // fresh coefficients (sim.cpp:245-246)
+    uint64_t count = 0;
+    for (size_t i = 0; i < c.species.size(); ++i) {
+      const float k = kinetic_energy(c, c.species[i], true);
+      kinetic[i] = k;
+      total += k;
+      count += c.species[i].n;
+    }
+    out->total_energy = total;
+    out->max_div_e_err = max_abs_lane(c, F_DIVE);
+    out->max_div_b_err = max_abs_lane(c, F_DIVB);
+    out->particle_count = count;
+  });
+}
+
 int pic_event_record(pic_context* ctx, int slot) {
   return guard([&] {
     Context& c = C_(ctx);

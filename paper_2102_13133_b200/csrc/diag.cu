@@ -1,0 +1,303 @@
+// Diagnostics on the device: the quantities
+// SimState::current_diagnostics / refresh_charge_diagnostics compute on the
+// diagnostic cadence (proj/src/sim.cpp:236-266, 230-234).
+//
+// Reference path restated (all /root/reference/proj):
+//   clear_rho                 src/fields.cpp:203-206
+//   deposit_rho               src/particles.cpp:384-410
+//   compute_div_errors        src/fields.cpp:253-274
+//   field_energy              src/fields.cpp:276-299 (+ sum_squares, kernels/scalar.cpp:51-59)
+//   max_abs_lane              src/fields.cpp:301-313
+//   kinetic_energy_centered   src/particles.cpp:468-501
+//   kinetic_energy            src/particles.cpp:460-466 (+ kinetic_sum, scalar.cpp:61-71)
+//
+// Parity: compute_div_errors and max_abs_lane are bit-exact (a stencil and an
+// order-free max).  The sums (energies, rho) are reassociated — the
+// reference itself changes them with its SIMD lane count and worker count —
+// so they are accumulated in fp64 on the device (energies) or with float
+// atomics (rho) and checked against the oracle within a stated tolerance.
+// Per-particle / per-voxel terms keep the reference's fp32 expressions.
+#include <algorithm>
+#include <cstring>
+
+#include "pic_device.cuh"
+#include "pic_internal.hpp"
+
+namespace picb {
+
+namespace {
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// Block reduction of two doubles into out[0..1] with one fp64 atomic each.
+__device__ __forceinline__ void block_add2(double a, double b, double* out) {
+  __shared__ double sa[32], sb[32];
+  a = warp_sum_d(a);
+  b = warp_sum_d(b);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) {
+    sa[w] = a;
+    sb[w] = b;
+  }
+  __syncthreads();
+  if (w == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    a = l < nw ? sa[l] : 0.0;
+    b = l < nw ? sb[l] : 0.0;
+    a = warp_sum_d(a);
+    b = warp_sum_d(b);
+    if (l == 0) {
+      atomicAdd(out, a);
+      atomicAdd(out + 1, b);
+    }
+  }
+}
+
+__device__ __forceinline__ void interior_of(const GridC& g, long long idx, int& ix, int& iy, int& iz) {
+  const long long nxy = (long long)g.nx * g.ny;
+  iz = (int)(idx / nxy);
+  const int r = (int)(idx - (long long)iz * nxy);
+  iy = r / g.nx;
+  ix = r - iy * g.nx + 1;
+  ++iy;
+  ++iz;
+}
+
+// field_energy: per interior voxel e = ex^2+ey^2+ez^2 (each v*v in fp32 as
+// sum_squares does), accumulated in fp64.
+__global__ void __launch_bounds__(256)
+field_energy_kernel(GridC g, const float* __restrict__ f, double* __restrict__ out) {
+  const long long n = (long long)g.nx * g.ny * g.nz;
+  const size_t V = (size_t)g.V;
+  double se = 0.0, sb = 0.0;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (long long)gridDim.x * blockDim.x) {
+    int ix, iy, iz;
+    interior_of(g, t, ix, iy, iz);
+    const size_t v = (size_t)voxel_of(g, ix, iy, iz);
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+      const float e = f[(size_t)(F_EX + l) * V + v];
+      const float b = f[(size_t)(F_BX + l) * V + v];
+      se += (double)(e * e);
+      sb += (double)(b * b);
+    }
+  }
+  block_add2(se, sb, out);
+}
+
+// max_abs_lane over the interior: |x| >= 0 orders like its bit pattern.
+__global__ void __launch_bounds__(256)
+max_abs_kernel(GridC g, const float* __restrict__ lane, unsigned* __restrict__ out) {
+  const long long n = (long long)g.nx * g.ny * g.nz;
+  unsigned m = 0;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+       t += (long long)gridDim.x * blockDim.x) {
+    int ix, iy, iz;
+    interior_of(g, t, ix, iy, iz);
+    const float a = fabsf(lane[voxel_of(g, ix, iy, iz)]);
+    const unsigned u = __float_as_uint(a);
+    m = (a > __uint_as_float(m)) ? u : m;  // NaN never replaces (fields.cpp:309 `v > m`)
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(kFull, m, o));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+// compute_div_errors (fields.cpp:253-274), same expression order.
+__global__ void __launch_bounds__(256)
+div_errors_kernel(GridC g, float* __restrict__ f, float rhx, float rhy, float rhz) {
+  const long long n = (long long)g.nx * g.ny * g.nz;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  int ix, iy, iz;
+  interior_of(g, t, ix, iy, iz);
+  const size_t V = (size_t)g.V;
+  const size_t v = (size_t)voxel_of(g, ix, iy, iz);
+  const size_t sx = 1, sy = (size_t)g.sy, sz = (size_t)g.sz;
+  const float* ex = f + (size_t)F_EX * V;
+  const float* ey = f + (size_t)F_EY * V;
+  const float* ez = f + (size_t)F_EZ * V;
+  const float* bx = f + (size_t)F_BX * V;
+  const float* by = f + (size_t)F_BY * V;
+  const float* bz = f + (size_t)F_BZ * V;
+  const float dive = ((ex[v] - ex[v - sx]) * rhx + (ey[v] - ey[v - sy]) * rhy) + (ez[v] - ez[v - sz]) * rhz;
+  f[(size_t)F_DIVE * V + v] = dive - f[(size_t)F_RHO * V + v];
+  f[(size_t)F_DIVB * V + v] =
+      ((bx[v + sx] - bx[v]) * rhx + (by[v + sy] - by[v]) * rhy) + (bz[v + sz] - bz[v]) * rhz;
+}
+
+// deposit_rho (particles.cpp:384-410): eight trilinear weights per particle
+// into the rhof lane.  Same-voxel lanes of a warp (the common case on a
+// voxel-sorted store) are summed with shuffles first; the adds into rhof
+// are float atomics (order not fixed: tolerance parity).
+__global__ void __launch_bounds__(256)
+deposit_rho_kernel(GridC g, const float4* __restrict__ pos, const float4* __restrict__ mom, long long n,
+                   float q, float scale, float* __restrict__ rho) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  int key = -1;
+  float w[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) w[k] = 0.f;
+  int ix = 0, iy = 0, iz = 0;
+  if (i < n) {
+    const float4 p = pos[i];
+    const float4 u = mom[i];
+    key = __float_as_int(p.w);
+    const unsigned rest = fast_div((unsigned)key, g.mag_pnx);
+    ix = key - (int)rest * g.pnx;
+    const unsigned izu = fast_div(rest, g.mag_pny);
+    iy = (int)rest - (int)izu * g.pny;
+    iz = (int)izu;
+    const float qw = (q * u.w) * scale;  // sp.q * w * scale (particles.cpp:393)
+    const float wxl = 1 - p.x, wxh = 1 + p.x;
+    const float wyl = 1 - p.y, wyh = 1 + p.y;
+    const float wzl = 1 - p.z, wzh = 1 + p.z;
+    w[0] = qw * (wxl * wyl * wzl);
+    w[1] = qw * (wxh * wyl * wzl);
+    w[2] = qw * (wxl * wyh * wzl);
+    w[3] = qw * (wxh * wyh * wzl);
+    w[4] = qw * (wxl * wyl * wzh);
+    w[5] = qw * (wxh * wyl * wzh);
+    w[6] = qw * (wxl * wyh * wzh);
+    w[7] = qw * (wxh * wyh * wzh);
+  }
+  // a warp that holds one voxel (the common case on a sorted store) sums its
+  // eight weights with a butterfly and lane 0 adds them; mixed warps add
+  // per particle.
+  const unsigned peers = __match_any_sync(kFull, key);
+  if (peers == kFull) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) w[k] += __shfl_xor_sync(kFull, w[k], o);
+    if (lane != 0) return;
+  }
+  if (key < 0) return;
+  const float* s = w;
+  const int xh = ix + 1 > g.nx ? 1 : ix + 1;
+  const int yh = iy + 1 > g.ny ? 1 : iy + 1;
+  const int zh = iz + 1 > g.nz ? 1 : iz + 1;
+  atomicAdd(rho + voxel_of(g, ix, iy, iz), s[0]);
+  atomicAdd(rho + voxel_of(g, xh, iy, iz), s[1]);
+  atomicAdd(rho + voxel_of(g, ix, yh, iz), s[2]);
+  atomicAdd(rho + voxel_of(g, xh, yh, iz), s[3]);
+  atomicAdd(rho + voxel_of(g, ix, iy, zh), s[4]);
+  atomicAdd(rho + voxel_of(g, xh, iy, zh), s[5]);
+  atomicAdd(rho + voxel_of(g, ix, yh, zh), s[6]);
+  atomicAdd(rho + voxel_of(g, xh, yh, zh), s[7]);
+}
+
+// kinetic_energy_centered (particles.cpp:468-501): momentum recentred by a
+// half electric kick with the current interpolators, (w m)(gamma - 1) per
+// particle in fp32, summed in fp64.  kCentered=false is kinetic_energy
+// (kinetic_sum, scalar.cpp:61-71).
+template <bool kCentered>
+__global__ void __launch_bounds__(256)
+kinetic_kernel(const float4* __restrict__ pos, const float4* __restrict__ mom, long long n,
+               const float4* __restrict__ interp, float qdt_2m, float m, double* __restrict__ out) {
+  double acc = 0.0;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float4 u = mom[i];
+    float cx = u.x, cy = u.y, cz = u.z;
+    if (kCentered) {
+      const float4 p = pos[i];
+      const float4* c = interp + (size_t)__float_as_int(p.w) * kInterpF4;
+      const float4 c0 = __ldg(c), c1 = __ldg(c + 1), c2 = __ldg(c + 2);
+      const float x = p.x, y = p.y, z = p.z;
+      const float ex = ((c0.x + y * c0.y) + z * c0.z) + (y * z) * c0.w;
+      const float ey = ((c1.x + z * c1.y) + x * c1.z) + (z * x) * c1.w;
+      const float ez = ((c2.x + x * c2.y) + y * c2.z) + (x * y) * c2.w;
+      cx = cx + qdt_2m * ex;
+      cy = cy + qdt_2m * ey;
+      cz = cz + qdt_2m * ez;
+    }
+    const float gm = __fsqrt_rn(1.0f + ((cx * cx + cy * cy) + cz * cz));
+    acc += (double)((u.w * m) * (gm - 1.0f));
+  }
+  block_add2(acc, 0.0, out);
+}
+
+unsigned grid_stride_blocks(const Context& c, long long n) {
+  const long long want = (n + 255) / 256;
+  const long long cap = (long long)c.num_sms * 8;
+  return (unsigned)std::max<long long>(1, std::min(want, cap));
+}
+
+}  // namespace
+
+void launch_clear_rho(Context& c) {
+  CUDA_OK(cudaMemsetAsync(c.f + (size_t)F_RHO * c.gc.V, 0, (size_t)c.gc.V * sizeof(float), c.stream));
+}
+
+void launch_deposit_rho(Context& c, Species& s) {
+  if (s.n == 0) return;
+  const float scale = 0.125f / ((c.grid.hx * c.grid.hy) * c.grid.hz);
+  deposit_rho_kernel<<<(unsigned)((s.n + 255) / 256), 256, 0, c.stream>>>(
+      c.gc, s.pos, s.mom, (long long)s.n, s.q, scale, c.f + (size_t)F_RHO * c.gc.V);
+  c.count_launch();
+}
+
+void launch_compute_div_errors(Context& c) {
+  const long long n = (long long)c.gc.nx * c.gc.ny * c.gc.nz;
+  div_errors_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(c.gc, c.f, 1.0f / c.grid.hx,
+                                                                      1.0f / c.grid.hy, 1.0f / c.grid.hz);
+  c.count_launch();
+}
+
+double* diag_slots(Context& c) {
+  return reinterpret_cast<double*>(c.scratch_bytes(Context::kScrDiag, 64 * sizeof(double)));
+}
+
+void field_energy(Context& c, float e_b[2]) {
+  double* d = diag_slots(c);
+  CUDA_OK(cudaMemsetAsync(d, 0, 2 * sizeof(double), c.stream));
+  const long long n = (long long)c.gc.nx * c.gc.ny * c.gc.nz;
+  field_energy_kernel<<<grid_stride_blocks(c, n), 256, 0, c.stream>>>(c.gc, c.f, d);
+  c.count_launch();
+  double h[2];
+  CUDA_OK(cudaMemcpyAsync(h, d, sizeof h, cudaMemcpyDeviceToHost, c.stream));
+  CUDA_OK(cudaStreamSynchronize(c.stream));
+  const double hv = 0.5 * (double)((c.grid.hx * c.grid.hy) * c.grid.hz);
+  e_b[0] = (float)(hv * h[0]);
+  e_b[1] = (float)(hv * h[1]);
+}
+
+float max_abs_lane(Context& c, int lane) {
+  unsigned* d = reinterpret_cast<unsigned*>(diag_slots(c) + 8);
+  CUDA_OK(cudaMemsetAsync(d, 0, sizeof(unsigned), c.stream));
+  const long long n = (long long)c.gc.nx * c.gc.ny * c.gc.nz;
+  max_abs_kernel<<<grid_stride_blocks(c, n), 256, 0, c.stream>>>(c.gc, c.f + (size_t)lane * c.gc.V, d);
+  c.count_launch();
+  unsigned h = 0;
+  CUDA_OK(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, c.stream));
+  CUDA_OK(cudaStreamSynchronize(c.stream));
+  float r;
+  std::memcpy(&r, &h, sizeof r);
+  return r;
+}
+
+float kinetic_energy(Context& c, Species& s, bool centered) {
+  if (s.n == 0) return 0.0f;
+  double* d = diag_slots(c) + 16;
+  CUDA_OK(cudaMemsetAsync(d, 0, 2 * sizeof(double), c.stream));
+  const float qdt_2m = (s.q * c.grid.dt) / (2.0f * s.m);
+  const unsigned b = grid_stride_blocks(c, (long long)s.n);
+  if (centered)
+    kinetic_kernel<true><<<b, 256, 0, c.stream>>>(s.pos, s.mom, (long long)s.n, c.interp, qdt_2m, s.m, d);
+  else
+    kinetic_kernel<false><<<b, 256, 0, c.stream>>>(s.pos, s.mom, (long long)s.n, c.interp, qdt_2m, s.m, d);
+  c.count_launch();
+  double h = 0;
+  CUDA_OK(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, c.stream));
+  CUDA_OK(cudaStreamSynchronize(c.stream));
+  return (float)h;
+}
+
+}  // namespace picb

@@ -61,16 +61,17 @@ struct Context {
   int* h_err = nullptr;       // pinned
   std::vector<Species> species;
   uint64_t launches = 0;
-  // advance_p strategy (push.cu): 7 = TMA-staged CTA rounds, 5 CTAs/SM (default);
+  // advance_p strategy (push.cu): 20 = run-per-lane, TMA in/out, 2 voxel slots (default);
+  // 7 = TMA-staged CTA rounds with warp reduction;
   // 0 = one particle per thread; 1, 5, 6, 8, 9 = TMA-staged ablations; 2-4 = other ablations
-  int push_variant = 7;
+  int push_variant = 20;
   int num_sms = 148;
   cudaEvent_t events[64] = {};
 
   enum ScratchSlot {
     kScrStage = 0, kScrNseg, kScrOff, kScrSegKey, kScrSegW,
     kScrKeyA, kScrValA, kScrKeyB, kScrValB, kScrHist, kScrScan,
-    kScrCount, kScrStart, kScrWithin, kScrStaging, kScrSmall, kScrN
+    kScrCount, kScrStart, kScrWithin, kScrStaging, kScrSmall, kScrDiag, kScrN
   };
   void* scratch[kScrN] = {};
   size_t scratch_size[kScrN] = {};
@@ -125,6 +126,14 @@ void launch_load_synthetic(Context& c, Species& s, int ppc, float u_th, const fl
                            uint64_t seed);
 void launch_interp_to_lanes(Context& c, float* out18);
 void launch_lanes_to_interp(Context& c, const float* in18);
+
+// ---- diagnostics (diag.cu) -----------------------------------------------------
+void launch_clear_rho(Context& c);
+void launch_deposit_rho(Context& c, Species& s);
+void launch_compute_div_errors(Context& c);
+void field_energy(Context& c, float e_b[2]);  // synchronous
+float max_abs_lane(Context& c, int lane);     // synchronous
+float kinetic_energy(Context& c, Species& s, bool centered);  // synchronous
 
 // ---- sort / scan primitives --------------------------------------------------
 int key_bits_for(long long max_key_exclusive);

@@ -144,7 +144,10 @@ def test_advance_p_parity(pic, orc, dims, n, u, deterministic):
     assert (wids != _push_case.ids0).mean() > 0.02
 
 
-@pytest.mark.parametrize("variant", range(10))
+PUSH_VARIANTS = list(range(30))
+
+
+@pytest.mark.parametrize("variant", PUSH_VARIANTS)
 def test_advance_p_strategies(pic, orc, variant):
     """Every advance_p deposit/tail strategy gives the bitwise particle state
     and the accumulator within tolerance."""
@@ -153,6 +156,36 @@ def test_advance_p_strategies(pic, orc, variant):
                                                     variant=variant)
     assert_bitwise(gids, wids, "ids")
     assert_bitwise(gp, wp, "particle lanes")
+    assert_close(gacc, wacc, ACC_RTOL, what="accumulator")
+
+
+@pytest.mark.parametrize("variant", [0, 7, 10, 11, 13, 17, 18, 19, 20, 21, 22])
+@pytest.mark.parametrize("dims,n,u,sort", [((40, 6, 5), 240000, 0.4, True), ((7, 6, 5), 30000, 1.2, False),
+                                           ((4, 3, 2), 31, 0.5, True)])
+def test_advance_p_strategies_layouts(pic, orc, variant, dims, n, u, sort):
+    """Sorted, unsorted (every particle a new voxel: slot evictions and a
+    full crossing queue) and tiny (partial TMA slices) stores."""
+    g = pic.make_grid(dims, 1.0, cfl_frac=0.9)
+    rng = np.random.default_rng(21)
+    o = og(g)
+    f = rand_fields(g, rng, scale=0.3, sync=lambda gg, ff: orc.ghost_sync(o, ff))
+    interp = orc.load_interpolators(o, f)
+    p, ids = rand_particles(g, rng, n, u_scale=u, sort=sort)
+    with pic.Context(g) as ctx:
+        sid = ctx.add_species("s", -1.0, 1.0, n)
+        ctx._set_push_variant(variant)
+        ctx.upload_species(sid, p, ids)
+        ctx.upload_fields(f)
+        ctx.load_interpolators()
+        ctx.clear_accumulator()
+        ctx.advance_p(sid)
+        ctx.synchronize()
+        gp, gids = ctx.download_species(sid)
+        gacc = ctx.download_accumulator()
+    wacc = np.zeros((g.padded, 12), np.float32)
+    orc.advance_particles(o, -1.0, 1.0, p, ids, interp, wacc, False)
+    assert_bitwise(gids, ids, "ids")
+    assert_bitwise(gp, p, "particle lanes")
     assert_close(gacc, wacc, ACC_RTOL, what="accumulator")
 
 
