@@ -266,6 +266,144 @@ def run_ours(args, rank, world):
                 push_ms_per_launch=push_ms_per_launch, nspecies=len(sids), grid=g, e2e=e2e)
 
 
+def run_ours_decomposed(args, rank, world):
+    """N > 1: weak-scaled slab decomposition.  The global box is
+    (n N) x n x n with each rank's slab the single-GPU deck; particles
+    migrate, the accumulator is halo-added and E/B halos copied over NCCL
+    (paper_2102_13133_b200/domain.py) every step."""
+    import torch
+
+    import paper_2102_13133_b200 as pic
+    from paper_2102_13133_b200.domain import CudaSlab, DecomposedSim, DistTransport, SlabGeometry
+
+    torch.cuda.set_device(args.device)
+    cfg = CONFIGS[args.config]
+    n = cfg["n"]
+    geom = SlabGeometry(n * world, n, n, world, h=(cfg["h"],) * 3, dt=cfg["dt"])
+    slab = CudaSlab(geom.local_grid(), rank, rank == 0, device=args.device)
+    sim = DecomposedSim(geom, {rank: slab}, DistTransport(rank, world))
+    ctx = slab.ctx
+    g = geom.local_grid()
+    sids = []
+    for name, q, m, ppc, uth, drift in cfg["species"]:
+        sid = sim.add_species(name, q, m, int(ppc * g.interior * 1.02) + 65536)
+        ctx.load_synthetic(sid, ppc, uth, drift, seed=1234 + 7919 * rank)
+        sids.append(sid)
+    ctx.synchronize()
+    sort_interval = cfg["sort_interval"]
+    step_count = [0]
+
+    def one_step():
+        sim.step()
+        step_count[0] += 1
+        if sort_interval > 0 and step_count[0] % sort_interval == 0:
+            for s_ in sids:
+                ctx.sort_particles(s_)
+
+    for s_ in sids:
+        ctx.sort_particles(s_)
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+    import torch.distributed as dist
+
+    stream = torch.cuda.current_stream()
+    clocks = ClockSampler(args.device)
+    clocks.start()
+    dist.barrier()
+    torch.cuda.synchronize()
+    l0 = ctx.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        one_step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = ctx.launch_count() - l0
+    clk = clocks.stop()
+    # push phase (advance_p of all species) timed with events per step
+    pev = []
+
+    def mark(phase, begin):
+        e = torch.cuda.Event(enable_timing=True)
+        e.record(stream)
+        pev.append(e)
+
+    sim.on_mark = mark
+    for _ in range(args.steps):
+        one_step()
+    sim.on_mark = None
+    torch.cuda.synchronize()
+    push_ms = sum(pev[2 * k].elapsed_time(pev[2 * k + 1]) for k in range(len(pev) // 2))
+    npart_local = sum(ctx.species_count(s_) for s_ in sids)
+    t = torch.tensor([ms, float(npart_local), push_ms], dtype=torch.float64, device="cuda")
+    mx = t.clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    sm = t.clone()
+    dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    ms = float(mx[0].item())
+    npart_total = int(sm[1].item())
+    push_ms_per_launch = float(mx[2].item()) / (args.steps * len(sids))
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e_decomposed(pic, sim, ctx, sids, args, world)
+    for e in sim.slabs.values():
+        e.ctx.close()
+    return dict(ms=ms, npart=npart_total // world, npart_total=npart_total, launches=launches, clocks=clk,
+                phases={"push": push_ms}, push_rate_kernel=npart_local * args.steps / (push_ms / 1e3),
+                push_ms_per_launch=push_ms_per_launch, nspecies=len(sids), grid=geom.global_grid(), e2e=e2e,
+                local_grid=g,
+                decomposed=True)
+
+
+def run_e2e_decomposed(pic, sim, ctx, sids, args, world):
+    """Decomposed host-buffer steps: every step uploads each rank's species
+    from pinned host records, runs the decomposed step, downloads them."""
+    import torch
+    import torch.distributed as dist
+    host = []
+    for s_ in sids:
+        cap = ctx.species_count(s_) + (1 << 20)
+        pos = np.zeros((cap, 4), np.float32)
+        mom = np.zeros((cap, 4), np.float32)
+        pic.host_register(pos)
+        pic.host_register(mom)
+        host.append([pos, mom, ctx.download_records(s_, pos, mom)])
+
+    def step():
+        b = 0
+        for s_, h in zip(sids, host):
+            ctx.upload_records(s_, h[0], h[1], h[2])
+            b += 32 * h[2]
+        sim.step()
+        for s_, h in zip(sids, host):
+            h[2] = ctx.download_records(s_, h[0], h[1])
+        return b
+
+    step()
+    dist.barrier()
+    k = max(1, args.e2e_steps)
+    t0 = time.perf_counter()
+    byt = 0
+    for _ in range(k):
+        byt += step()
+    dt = time.perf_counter() - t0
+    t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dt = float(t.item())
+    npart = sum(h[2] for h in host)
+    tn = torch.tensor([float(npart)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(tn)
+    for h in host:
+        pic.host_unregister(h[0])
+        pic.host_unregister(h[1])
+    return {"value": float(tn.item()) * k / dt, "unit": "particle pushes/s", "h2d_bytes_per_step": byt // k,
+            "d2h_bytes_per_step": byt // k, "steps": k, "ms_per_step": dt / k * 1e3,
+            "note": "per rank: records H2D, decomposed step, records D2H (not pipelined); bytes are rank 0's"}
+
+
 def run_e2e(pic, ctx, sids, npart, args, world):
     """pic_step_host: every step uploads all species from pinned host
     buffers, steps, and downloads them back (32 B/particle each way)."""
@@ -309,6 +447,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-n", type=int, default=64)
+    ap.add_argument("--decomposed", action="store_true",
+                    help="use the slab-decomposed (NCCL) step even at N=1 (self-exchange; tests the N>1 path)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -338,12 +478,18 @@ def main():
         print(json.dumps(line))
         return
 
-    if world > 1:
+    if world > 1 or args.decomposed:
         import torch
         import torch.distributed as dist
-        dist.init_process_group("gloo")  # control plane only (barrier + max-reduce of timings)
-
-    res = run_ours(args, rank, world)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        res = run_ours_decomposed(args, rank, world)
+    else:
+        res = run_ours(args, rank, world)
     if rank != 0:
         if world > 1:
             import torch.distributed as dist
@@ -351,12 +497,12 @@ def main():
         return
 
     ms_per_step = res["ms"] / args.steps
-    value = res["npart"] * world * args.steps / (res["ms"] / 1e3)
+    value = res.get("npart_total", res["npart"] * world) * args.steps / (res["ms"] / 1e3)
     peak, peak_kind = measured_peak_gbs()
     achieved = res["npart"] / res["nspecies"] * BYTES_PER_PUSH / (res["push_ms_per_launch"] / 1e3) / 1e9
     prof = profile_traffic()
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only
         try:
             r = cpu_reference(args.config, 3, 1, sample_n=args.cpu_sample_n)
             if r:
@@ -364,6 +510,7 @@ def main():
         except Exception as e:  # the baseline is reported, not required
             cpu = {"value": None, "error": str(e)[:200]}
     g = res["grid"]
+    gl = res.get("local_grid", g)
     line = {
         "metric": "particle pushes/sec/GPU (advance_p, whole step)",
         "value": value,
@@ -377,9 +524,11 @@ def main():
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (device counter-RNG load: uniform offsets, drifting Maxwellian momenta)",
-        "config": {"workload": args.config, "cells": f"{g.nx}x{g.ny}x{g.nz}", "particles_per_gpu": res["npart"],
+        "config": {"workload": args.config, "cells": f"{gl.nx}x{gl.ny}x{gl.nz}", "particles_per_gpu": res["npart"],
                    "ppc": sum(s[3] for s in cfg["species"]), "dt": g.dt, "sort_interval": cfg["sort_interval"],
-                   "parallelism": "replicas" if world > 1 else "single",
+                   "parallelism": f"x-slab decomposition over {world} GPUs (NCCL halo + migration)"
+                   if res.get("decomposed") else "single",
+                   "global_cells": f"{g.nx}x{g.ny}x{g.nz}",
                    "l2": "inputs (34 GB of particle records) >> 126 MB L2; no flush",
                    "push_kernel_rate": res["push_rate_kernel"],
                    "phase_ms_per_step": {k: v / args.steps for k, v in res["phases"].items()}},
@@ -397,7 +546,7 @@ def main():
         "clocks": res["clocks"],
     }
     print(json.dumps(line))
-    if world > 1:
+    if world > 1 or args.decomposed:
         import torch.distributed as dist
         dist.destroy_process_group()
 

@@ -148,6 +148,42 @@ int pic_step(pic_context* ctx, unsigned flags);
 int pic_step_host(pic_context* ctx, unsigned flags, float* const* lanes7,
                   int32_t* const* ids);
 
+/* ---- domain decomposition in x -------------------------------
+ * A slab of a global periodic box decomposed along x.  With x_open set the
+ * context's x faces stop being periodic (the single-domain wrap of
+ * particles.cpp:348-350 / grid.cpp:32-52, the x pass of ghost_fold_currents,
+ * grid.cpp:78-86, and the x pass of ghost_sync_fields, fields.cpp:35-44);
+ * the host exchanges x planes and migrating particles with its neighbours
+ * (NCCL through torch.distributed in paper_2102_13133_b200/domain.py) using
+ * the pack / unpack calls below.  low_wraps: this slab's low x face is the
+ * global periodic boundary (fixes the reference's unload sum order there).
+ * Slabs must have equal nx.  pic_step / pic_step_host refuse an x-open
+ * context: the host sequences the step around the exchanges. */
+int pic_set_x_open(pic_context* ctx, int x_open, int low_wraps);
+/* Runs the context's work on a caller-provided cudaStream_t (a created
+ * stream, e.g. torch's current stream, so NCCL send/recv order with the
+ * kernels); NULL restores the context's own stream (the legacy default
+ * stream cannot be borrowed). */
+int pic_set_stream(pic_context* ctx, void* cuda_stream);
+/* Halo planes: kind 0 = accumulator rows (12 floats per voxel), 1 = E and B
+ * (6 floats), 2 = rhof (1 float); a plane is every (iy, iz) of the padded
+ * y-z range at x index ix in [0, nx + 1].  Device buffers. */
+#define PIC_HALO_ACCUMULATOR 0
+#define PIC_HALO_FIELDS 1
+#define PIC_HALO_RHO 2
+int pic_halo_plane_bytes(pic_context* ctx, int kind, size_t* out);
+int pic_halo_pack(pic_context* ctx, int kind, int ix, void* dst_dev, int zero_after);
+int pic_halo_unpack(pic_context* ctx, int kind, int ix, const void* src_dev, int accumulate);
+/* Migration after an x-open pic_advance_p: emigrant counts through the low
+ * and high x faces (a quiescence point), then pack them — 32-byte device
+ * records (pos float4, mom float4), voxel ids already in the receiving
+ * slab's frame, ascending particle index — into two device buffers while
+ * the store is compacted (holes filled from the tail in index order), then
+ * append received records at the end of the store. */
+int pic_migrate_counts(pic_context* ctx, int species, size_t out_counts[2]);
+int pic_migrate_pack(pic_context* ctx, int species, void* low_dev, void* high_dev);
+int pic_migrate_append(pic_context* ctx, int species, const void* records_dev, size_t count);
+
 /* ---- diagnostics -------------------------------------
  * The diagnostic-cadence quantities of SimState::refresh_charge_diagnostics /
  * current_diagnostics (proj/src/sim.cpp:230-266).  compute_div_errors and

@@ -30,6 +30,11 @@ FIELD_LANES = ["ex", "ey", "ez", "div_e_err", "cbx", "cby", "cbz", "div_b_err",
                "jfx", "jfy", "jfz", "rhof", "tcax", "tcay", "tcaz", "rhob"]
 F = {name: i for i, name in enumerate(FIELD_LANES)}
 
+# halo plane kinds (pic_b200.h)
+HALO_ACCUMULATOR = 0
+HALO_FIELDS = 1
+HALO_RHO = 2
+
 
 class PicError(RuntimeError):
     code = 5
@@ -148,6 +153,14 @@ def lib() -> C.CDLL:
         "pic_max_abs_lane": [P, C.c_int, C.POINTER(C.c_float)],
         "pic_kinetic_energy": [P, C.c_int, C.c_int, C.POINTER(C.c_float)],
         "pic_diagnostics": [P, C.POINTER(Diag), C.POINTER(C.c_float), C.c_size_t],
+        "pic_set_x_open": [P, C.c_int, C.c_int],
+        "pic_set_stream": [P, P],
+        "pic_halo_plane_bytes": [P, C.c_int, C.POINTER(C.c_size_t)],
+        "pic_halo_pack": [P, C.c_int, C.c_int, P, C.c_int],
+        "pic_halo_unpack": [P, C.c_int, C.c_int, P, C.c_int],
+        "pic_migrate_counts": [P, C.c_int, C.POINTER(C.c_size_t)],
+        "pic_migrate_pack": [P, C.c_int, P, P],
+        "pic_migrate_append": [P, C.c_int, P, C.c_size_t],
     }
     for name, argtypes in sigs.items():
         fn = getattr(L, name)
@@ -229,6 +242,17 @@ class Context:
         check(lib().pic_species_download(self._h, sid, p, ids))
         return p, ids
 
+    def upload_records(self, sid: int, pos16: np.ndarray, mom16: np.ndarray, n: int):
+        """Native 32-byte records: pos/mom float32 arrays of shape (>= n, 4)."""
+        assert pos16.dtype == np.float32 and mom16.dtype == np.float32 and pos16.shape[0] >= n
+        check(lib().pic_species_upload_records(self._h, sid, n, pos16.ctypes.data, mom16.ctypes.data))
+
+    def download_records(self, sid: int, pos16: np.ndarray, mom16: np.ndarray) -> int:
+        n = self.species_count(sid)
+        assert pos16.shape[0] >= n and mom16.shape[0] >= n
+        check(lib().pic_species_download_records(self._h, sid, pos16.ctypes.data, mom16.ctypes.data))
+        return n
+
     def load_synthetic(self, sid: int, ppc: int, u_th: float, drift=(0.0, 0.0, 0.0), seed: int = 1):
         check(lib().pic_species_load_synthetic(self._h, sid, ppc, u_th, np.asarray(drift, np.float32), seed))
 
@@ -308,6 +332,37 @@ class Context:
 
     def synchronize(self):
         check(lib().pic_synchronize(self._h))
+
+    # --- domain decomposition in x (device pointers) ------------------
+    def set_x_open(self, x_open: bool = True, low_wraps: bool = False):
+        check(lib().pic_set_x_open(self._h, int(x_open), int(low_wraps)))
+
+    def set_stream(self, cuda_stream_ptr):
+        """Run on a caller's cudaStream_t (an int handle, e.g.
+        torch.cuda.current_stream().cuda_stream); None restores our own."""
+        check(lib().pic_set_stream(self._h, C.c_void_p(cuda_stream_ptr) if cuda_stream_ptr else None))
+
+    def halo_plane_bytes(self, kind: int) -> int:
+        n = C.c_size_t()
+        check(lib().pic_halo_plane_bytes(self._h, kind, C.byref(n)))
+        return n.value
+
+    def halo_pack(self, kind: int, ix: int, dst_ptr: int, zero_after: bool = False):
+        check(lib().pic_halo_pack(self._h, kind, ix, C.c_void_p(dst_ptr), int(zero_after)))
+
+    def halo_unpack(self, kind: int, ix: int, src_ptr: int, accumulate: bool = False):
+        check(lib().pic_halo_unpack(self._h, kind, ix, C.c_void_p(src_ptr), int(accumulate)))
+
+    def migrate_counts(self, sid: int):
+        out = (C.c_size_t * 2)()
+        check(lib().pic_migrate_counts(self._h, sid, out))
+        return int(out[0]), int(out[1])
+
+    def migrate_pack(self, sid: int, low_ptr: int, high_ptr: int):
+        check(lib().pic_migrate_pack(self._h, sid, C.c_void_p(low_ptr), C.c_void_p(high_ptr)))
+
+    def migrate_append(self, sid: int, src_ptr: int, count: int):
+        check(lib().pic_migrate_append(self._h, sid, C.c_void_p(src_ptr), count))
 
     # --- diagnostics (proj/src/sim.cpp:230-266) ---------------------------------
     def clear_rho(self):

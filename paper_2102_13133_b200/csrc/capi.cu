@@ -72,11 +72,14 @@ void Context::resolve_phases() {
 
 void Context::release() {
   if (stream) cudaStreamSynchronize(stream);
+  if (own_stream && stream != own_stream) cudaStreamSynchronize(own_stream);
   for (auto& s : species) {
     cudaFree(s.pos);
     cudaFree(s.mom);
     cudaFree(s.pos_alt);
     cudaFree(s.mom_alt);
+    cudaFree(s.mig_idx);
+    cudaFree(s.mig_count);
   }
   species.clear();
   for (int i = 0; i < kScrN; ++i) {
@@ -105,6 +108,7 @@ void Context::release() {
   if (cs_in) cudaStreamDestroy(cs_in);
   if (cs_out) cudaStreamDestroy(cs_out);
   cs_in = cs_out = nullptr;
+  if (own_stream) stream = own_stream;  // never destroy a borrowed stream
   if (stream) cudaStreamDestroy(stream);
   f = nullptr;
   interp = nullptr;
@@ -112,6 +116,7 @@ void Context::release() {
   d_err = nullptr;
   h_err = nullptr;
   stream = nullptr;
+  own_stream = nullptr;
 }
 
 // validate_grid / cfl_limit (proj/src/grid.cpp:7-20), in fp32.
@@ -641,6 +646,7 @@ int pic_sort_particles(pic_context* ctx, int species, int order) {
 }
 int pic_step(pic_context* ctx, unsigned flags) {
   return guard([&] {
+    if (C_(ctx).gc.xopen) throw UsageError("pic_step: x-open (decomposed) context; the host sequences the step");
     step(C_(ctx), flags);
     check_launch();
   });
@@ -649,6 +655,7 @@ int pic_step(pic_context* ctx, unsigned flags) {
 int pic_step_host(pic_context* ctx, unsigned flags, float* const* lanes7, int32_t* const* ids) {
   return guard([&] {
     Context& c = C_(ctx);
+    if (c.gc.xopen) throw UsageError("pic_step_host: x-open (decomposed) context");
     if (flags & PIC_DETERMINISTIC) {
       // ordered replay needs whole-species passes: upload, step, download
       for (size_t s = 0; s < c.species.size(); ++s) {
@@ -675,6 +682,53 @@ int pic_step_host(pic_context* ctx, unsigned flags, float* const* lanes7, int32_
     }
     check_launch();
     quiesce(c);
+  });
+}
+
+int pic_set_x_open(pic_context* ctx, int x_open, int low_wraps) {
+  return guard([&] { set_x_open(C_(ctx), x_open != 0, low_wraps != 0); });
+}
+int pic_set_stream(pic_context* ctx, void* cuda_stream) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    CUDA_OK(cudaStreamSynchronize(c.stream));
+    if (!c.own_stream) c.own_stream = c.stream;
+    c.stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : c.own_stream;
+  });
+}
+int pic_halo_plane_bytes(pic_context* ctx, int kind, size_t* out) {
+  return guard([&] { *out = halo_plane_bytes(C_(ctx), kind); });
+}
+int pic_halo_pack(pic_context* ctx, int kind, int ix, void* dst_dev, int zero_after) {
+  return guard([&] {
+    halo_pack(C_(ctx), kind, ix, dst_dev, zero_after != 0);
+    check_launch();
+  });
+}
+int pic_halo_unpack(pic_context* ctx, int kind, int ix, const void* src_dev, int accumulate) {
+  return guard([&] {
+    halo_unpack(C_(ctx), kind, ix, src_dev, accumulate != 0);
+    check_launch();
+  });
+}
+int pic_migrate_counts(pic_context* ctx, int species, size_t out_counts[2]) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    quiesce(c);
+    migrate_counts(c, species_at(c, species), out_counts);
+  });
+}
+int pic_migrate_pack(pic_context* ctx, int species, void* low_dev, void* high_dev) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    migrate_pack(c, species_at(c, species), low_dev, high_dev);
+    check_launch();
+  });
+}
+int pic_migrate_append(pic_context* ctx, int species, const void* records_dev, size_t count) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    migrate_append(c, species_at(c, species), records_dev, count);
   });
 }
 

@@ -148,10 +148,13 @@ unload_advance_e_kernel(GridC g, Lanes L, const float* __restrict__ acc, ECoef k
   const size_t v = (size_t)voxel_of(g, ix, iy, iz);
   float jx = L.p[F_JX][v], jy = L.p[F_JY][v], jz = L.p[F_JZ][v];
   if (kUnload) {
-    const int xm = ix == 1 ? g.nx : ix - 1;
+    // x-decomposed: the x-1 neighbour of ix = 1 is the ghost plane filled
+    // from the low neighbour; it precedes in the reference's sum order
+    // unless this slab's low face is the global periodic boundary
+    const int xm = (ix == 1 && !g.xopen) ? g.nx : ix - 1;
     const int ym = iy == 1 ? g.ny : iy - 1;
     const int zm = iz == 1 ? g.nz : iz - 1;
-    const bool xmf = ix != 1, ymf = iy != 1, zmf = iz != 1;
+    const bool xmf = ix != 1 || (g.xopen && !g.x_low_wraps), ymf = iy != 1, zmf = iz != 1;
     const float* a_000 = acc + (size_t)v * 12;
     const float* a_0y0 = acc + (size_t)voxel_of(g, ix, ym, iz) * 12;
     const float* a_00z = acc + (size_t)voxel_of(g, ix, iy, zm) * 12;
@@ -192,7 +195,8 @@ __device__ __forceinline__ int wrapc(int i, int n) { return i == 0 ? n : (i == n
 __global__ void __launch_bounds__(256)
 ghost_sync_kernel(GridC g, Lanes L) {
   long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long fx = 2LL * g.pny * g.pnz, fy = 2LL * g.pnx * g.pnz, fz = 2LL * g.pnx * g.pny;
+  // x-decomposed: the x faces come from the neighbours (halo exchange)
+  const long long fx = g.xopen ? 0 : 2LL * g.pny * g.pnz, fy = 2LL * g.pnx * g.pnz, fz = 2LL * g.pnx * g.pny;
   int ix, iy, iz;
   if (t < fx) {
     const int side = (int)(t & 1);
@@ -216,7 +220,7 @@ ghost_sync_kernel(GridC g, Lanes L) {
     return;
   }
   const size_t to = (size_t)voxel_of(g, ix, iy, iz);
-  const size_t from = (size_t)voxel_of(g, wrapc(ix, g.nx), wrapc(iy, g.ny), wrapc(iz, g.nz));
+  const size_t from = (size_t)voxel_of(g, g.xopen ? ix : wrapc(ix, g.nx), wrapc(iy, g.ny), wrapc(iz, g.nz));
   L.p[F_EX][to] = L.p[F_EX][from];
   L.p[F_EY][to] = L.p[F_EY][from];
   L.p[F_EZ][to] = L.p[F_EZ][from];
@@ -388,10 +392,14 @@ void launch_ghost_sync(Context& c) {
 void launch_ghost_fold(Context& c) {
   const GridC& g = c.gc;
   const long long nx = (long long)g.pny * g.pnz, ny = (long long)g.nx * g.pnz, nz = (long long)g.nx * g.ny;
-  fold_x_kernel<<<(unsigned)((nx + 255) / 256), 256, 0, c.stream>>>(g, c.acc);
+  // x-decomposed: the x planes were folded into the neighbours by exchange
+  if (!g.xopen) {
+    fold_x_kernel<<<(unsigned)((nx + 255) / 256), 256, 0, c.stream>>>(g, c.acc);
+    c.count_launch();
+  }
   fold_y_kernel<<<(unsigned)((ny + 255) / 256), 256, 0, c.stream>>>(g, c.acc);
   fold_z_kernel<<<(unsigned)((nz + 255) / 256), 256, 0, c.stream>>>(g, c.acc);
-  c.count_launch(3);
+  c.count_launch(2);
 }
 
 void launch_clear_currents(Context& c) {

@@ -20,6 +20,7 @@ enum ErrBits : int {
   kErrMover = 2,     // mover did not terminate in 8 passes (:240)
   kErrWrap = 4,      // final voxel beyond one cell (proj/src/grid.cpp:42-43)
   kErrVoxel = 8,     // voxel id outside the padded lattice (grid.cpp:33-34)
+  kErrMigCap = 16,   // emigrant list overflow (domain decomposition)
 };
 
 // GridDescriptor (proj/include/minipic/grid.hpp:15-38) plus derived strides.
@@ -32,6 +33,12 @@ struct GridC {
   // exact division by pnx / pny: floor(v / d) == __umul64hi(v, m) with
   // m = ceil(2^64 / d), valid for 0 <= v < 2^31 (host computes m).
   unsigned long long mag_pnx, mag_pny;
+  // Domain decomposition in x: with xopen the x faces are not
+  // periodic — particles leaving through them become emigrants, the x ghost
+  // planes are filled / folded by neighbour exchange instead of wrap-around.
+  // x_low_wraps: this slab's low face is the global periodic boundary
+  // (rank 0), which fixes the summation order of the wrapped unload edge.
+  int xopen, x_low_wraps;
 };
 
 __device__ __forceinline__ unsigned fast_div(unsigned v, unsigned long long m) {

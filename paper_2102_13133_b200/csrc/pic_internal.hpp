@@ -47,6 +47,11 @@ struct Species {
   float4* mom = nullptr;  // (ux, uy, uz, w)
   float4* pos_alt = nullptr;  // permutation target of the sort (lazy)
   float4* mom_alt = nullptr;
+  // x-decomposition: emigrant index lists of the last push (low / high
+  // face), capacity mig_cap each; mig_count[2] on the device (lazy)
+  unsigned* mig_count = nullptr;
+  unsigned* mig_idx = nullptr;
+  unsigned mig_cap = 0;
 };
 
 struct Context {
@@ -54,6 +59,7 @@ struct Context {
   pic_grid grid{};
   GridC gc{};
   cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;  // set when pic_set_stream borrowed a stream
   float* f = nullptr;         // 16 lanes x V, lane-major
   float4* interp = nullptr;   // V x 5 float4
   float* acc = nullptr;       // V x 12
@@ -71,7 +77,7 @@ struct Context {
   enum ScratchSlot {
     kScrStage = 0, kScrNseg, kScrOff, kScrSegKey, kScrSegW,
     kScrKeyA, kScrValA, kScrKeyB, kScrValB, kScrHist, kScrScan,
-    kScrCount, kScrStart, kScrWithin, kScrStaging, kScrSmall, kScrDiag, kScrN
+    kScrCount, kScrStart, kScrWithin, kScrStaging, kScrSmall, kScrDiag, kScrMigA, kScrMigB, kScrMigC, kScrMigT, kScrN
   };
   void* scratch[kScrN] = {};
   size_t scratch_size[kScrN] = {};
@@ -126,6 +132,21 @@ void launch_load_synthetic(Context& c, Species& s, int ppc, float u_th, const fl
                            uint64_t seed);
 void launch_interp_to_lanes(Context& c, float* out18);
 void launch_lanes_to_interp(Context& c, const float* in18);
+
+// ---- domain decomposition in x (domain.cu) -----------------------
+void ensure_mig_lists(Context& c, Species& s);
+void set_x_open(Context& c, bool open, bool low_wraps);
+// halo planes: kind 0 = accumulator (12 lanes / voxel), 1 = E and B
+// (6 lanes), 2 = rhof; one x plane covers all (iy, iz) incl. ghosts
+size_t halo_plane_bytes(const Context& c, int kind);
+void halo_pack(Context& c, int kind, int ix, void* dst, bool zero_after);
+void halo_unpack(Context& c, int kind, int ix, const void* src, bool accumulate);
+// migration after an x-open push: counts of emigrants through the low /
+// high face (synchronous), then pack (32 B device records, ids translated
+// to the neighbour's frame) + compact, then append received records
+void migrate_counts(Context& c, Species& s, size_t out[2]);
+void migrate_pack(Context& c, Species& s, void* low_dst, void* high_dst);
+void migrate_append(Context& c, Species& s, const void* src, size_t count);
 
 // ---- diagnostics (diag.cu) -----------------------------------------------------
 void launch_clear_rho(Context& c);
