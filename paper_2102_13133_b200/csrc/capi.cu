@@ -155,6 +155,7 @@ Context* make_context(int device, const pic_grid& g) {
     CUDA_OK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CUDA_OK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     if (const char* v = std::getenv("PIC_PUSH_VARIANT")) c->push_variant = std::atoi(v);  // profiling knob
+    if (const char* v = std::getenv("PIC_SORT_VARIANT")) c->sort_variant = std::atoi(v);  // profiling knob
     const size_t V = (size_t)gc.V;
     CUDA_OK(cudaMalloc(&c->f, F_COUNT * V * sizeof(float)));
     CUDA_OK(cudaMalloc(&c->interp, kInterpF4 * V * sizeof(float4)));
@@ -846,6 +847,15 @@ int pic_phase_timings(pic_context* ctx, double out_ms[5], int reset) {
 }
 
 // Not in the public header: selects an advance_p strategy (benchmarking).
+int pic_internal_set_sort_variant(pic_context* ctx, int variant) {
+  // variant: 0 = radix with 9-bit digits (default), 1 = tiled counting
+  // sort, 2 = radix with 8-bit digits (benchmarking hook)
+  return guard([&] {
+    Context& c = C_(ctx);
+    c.sort_variant = variant == 1 ? 1 : 0;
+    c.sort_radix_bits = variant == 2 ? 8 : 9;
+  });
+}
 int pic_internal_set_push_variant(pic_context* ctx, int variant) {
   return guard([&] { C_(ctx).push_variant = variant; });
 }

@@ -67,10 +67,14 @@ struct Context {
   int* h_err = nullptr;       // pinned
   std::vector<Species> species;
   uint64_t launches = 0;
-  // advance_p strategy (push.cu): 20 = run-per-lane, TMA in/out, 2 voxel slots (default);
+  // advance_p strategy (push.cu): 30 = run-per-lane, TMA in/out, 2 voxel slots holding
+  // first-segment moments (default); 20 = the same with per-particle weights;
   // 7 = TMA-staged CTA rounds with warp reduction;
   // 0 = one particle per thread; 1, 5, 6, 8, 9 = TMA-staged ablations; 2-4 = other ablations
-  int push_variant = 20;
+  int push_variant = 30;
+  // sort_particles (blocked): 0 = LSD radix over (voxel, index), 1 = tiled counting sort (ablation)
+  int sort_variant = 0;
+  int sort_radix_bits = 9;  // LSD digit width (passes = ceil(key bits / width), widths evened out)
   int num_sms = 148;
   cudaEvent_t events[64] = {};
 
