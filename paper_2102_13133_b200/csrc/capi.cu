@@ -846,16 +846,16 @@ int pic_phase_timings(pic_context* ctx, double out_ms[5], int reset) {
   });
 }
 
-// Not in the public header: selects an advance_p strategy (benchmarking).
+// Not in the public header: sort strategy (benchmarking): 0 = radix with
+// 8-bit digits (default), 1 = tiled counting sort, 2 = radix, 9-bit digits.
 int pic_internal_set_sort_variant(pic_context* ctx, int variant) {
-  // variant: 0 = radix with 9-bit digits (default), 1 = tiled counting
-  // sort, 2 = radix with 8-bit digits (benchmarking hook)
   return guard([&] {
     Context& c = C_(ctx);
     c.sort_variant = variant == 1 ? 1 : 0;
-    c.sort_radix_bits = variant == 2 ? 8 : 9;
+    c.sort_radix_bits = variant == 2 ? 9 : 8;
   });
 }
+// Not in the public header: selects an advance_p strategy (benchmarking).
 int pic_internal_set_push_variant(pic_context* ctx, int variant) {
   return guard([&] { C_(ctx).push_variant = variant; });
 }

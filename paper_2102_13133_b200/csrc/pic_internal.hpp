@@ -74,7 +74,7 @@ struct Context {
   int push_variant = 30;
   // sort_particles (blocked): 0 = LSD radix over (voxel, index), 1 = tiled counting sort (ablation)
   int sort_variant = 0;
-  int sort_radix_bits = 9;  // LSD digit width (passes = ceil(key bits / width), widths evened out)
+  int sort_radix_bits = 8;  // LSD digit width (passes = ceil(key bits / width), widths evened out)
   int num_sms = 148;
   cudaEvent_t events[64] = {};
 

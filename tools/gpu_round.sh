@@ -1,0 +1,13 @@
+#!/bin/bash
+# Full one-GPU measurement pass: tests, smoke, bench lines (two-stream headline,
+# thermal, decomposed self-exchange), launch list, ncu --set full of the
+# default advance_p at a fresh and a stale launch.
+TAG=${1:-r1}
+set -x
+timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/gputest_$TAG.log 2>&1; tail -3 gpurun_out/gputest_$TAG.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; tail -2 gpurun_out/smoke_$TAG.log
+bash tools/gpu_bench.sh $TAG > gpurun_out/bench_$TAG.log 2>&1
+timeout 900 python bench.py --decomposed --steps 20 --warmup 4 --no-cpu-baseline --no-e2e > gpurun_out/bench_dec_$TAG.json 2> gpurun_out/bench_dec_$TAG.err
+bash tools/gpu_ncu_stale.sh $TAG 30:0 30:38
+for f in gpurun_out/prof_${TAG}_v30_s*.ncu-rep; do python tools/ncu_summary.py $f 536870912 > ${f%.ncu-rep}.txt; python tools/ncu_lines.py $f 40 >> ${f%.ncu-rep}.txt; done
+ls gpurun_out
