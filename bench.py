@@ -431,9 +431,10 @@ def run_e2e(pic, ctx, sids, npart, args, world):
     for p, ids in host:
         pic.host_unregister(p)
         pic.host_unregister(ids)
-    b = sum(h[0].nbytes + h[1].nbytes for h in host)
-    return {"value": npart * k * world / dt, "unit": "particle pushes/s", "h2d_bytes_per_step": b,
-            "d2h_bytes_per_step": b, "steps": k, "ms_per_step": dt / k * 1e3}
+    b_in = sum(h[0].nbytes + h[1].nbytes for h in host)
+    b_out = sum(h[0].nbytes * 6 // 7 + h[1].nbytes for h in host)  # lanes 0-5 + ids (w is not modified)
+    return {"value": npart * k * world / dt, "unit": "particle pushes/s", "h2d_bytes_per_step": b_in,
+            "d2h_bytes_per_step": b_out, "steps": k, "ms_per_step": dt / k * 1e3}
 
 
 def main():

@@ -144,7 +144,10 @@ int pic_sort_particles(pic_context* ctx, int species, int order);
 int pic_step(pic_context* ctx, unsigned flags);
 /* The same step with host-resident species (the reference's host
  * advance_particles contract): uploads every species from lanes7[s]/ids[s],
- * steps, downloads back into the same buffers. */
+ * steps, downloads back into the same buffers (the weight lane, which the
+ * step never modifies, is not copied back).  Species stream through the
+ * device in chunks with H2D, compute and D2H overlapped; pin the buffers
+ * (pic_host_register) for the copies to overlap. */
 int pic_step_host(pic_context* ctx, unsigned flags, float* const* lanes7,
                   int32_t* const* ids);
 

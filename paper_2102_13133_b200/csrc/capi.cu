@@ -309,7 +309,9 @@ static void step_host(Context& c, unsigned flags, float* const* lanes7, int32_t*
       CUDA_OK(cudaEventRecord(c.ev_unpacked[b], c.stream));
       // D2H
       CUDA_OK(cudaStreamWaitEvent(c.cs_out, c.ev_unpacked[b], 0));
-      CUDA_OK(cudaMemcpy2DAsync(lanes7[si] + start, n * 4, out, cnt * 4, cnt * 4, 7, cudaMemcpyDeviceToHost,
+      // the push never changes the weight lane (particles.cpp:255-360): rows
+      // 0-5 (offsets, momenta) and the ids come back, w stays as the host has it
+      CUDA_OK(cudaMemcpy2DAsync(lanes7[si] + start, n * 4, out, cnt * 4, cnt * 4, 6, cudaMemcpyDeviceToHost,
                                 c.cs_out));
       CUDA_OK(cudaMemcpyAsync(ids[si] + start, out + cnt * 28, cnt * 4, cudaMemcpyDeviceToHost, c.cs_out));
       CUDA_OK(cudaEventRecord(c.ev_out[b], c.cs_out));
