@@ -53,6 +53,12 @@ CONFIGS = {
     "thermal": dict(n=64, h=1.0, dt=0.25, sort_interval=20,
                     species=[("electron", -0.125, 0.125, 32, 0.1, (0.0, 0.0, 0.0)),
                              ("ion", 0.125, 12.5, 32, 0.01, (0.0, 0.0, 0.0))]),
+    # diagnostic only: the two-stream beams with a negligible charge
+    # (ballistic drift, no field growth) to separate sort staleness from
+    # the deck's physics in push timings
+    "two_stream_ballistic": dict(n=256, h=1.0, dt=0.25, sort_interval=20,
+                                 species=[("beam_p", -1e-20, 1.0 / 64, 32, 0.01, (0.2, 0.0, 0.0)),
+                                          ("beam_m", -1e-20, 1.0 / 64, 32, 0.01, (-0.2, 0.0, 0.0))]),
     # configs[4]: weak scaling uniform plasma, ~1e9 particles per GPU
     "weak": dict(n=256, h=1.0, dt=0.25, sort_interval=20,
                  species=[("electron", -0.125, 0.125, 32, 0.1, (0.0, 0.0, 0.0)),
