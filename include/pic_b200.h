@@ -223,6 +223,50 @@ typedef struct pic_diag {
  * current div errors, as SimState::run does on the diag cadence. */
 int pic_diagnostics(pic_context* ctx, pic_diag* out, float* kinetic, size_t kinetic_cap);
 
+/* ---- decks and the SimState run surface ---------------
+ * The reference's host API above the step: the deck text format
+ * (proj/src/deck.cpp:20-395), SimState::initialize / step / run /
+ * emit_diagnostics (proj/src/sim.cpp:25-47, 74-134, 143-306) and the binary
+ * field dump (proj/src/fields.cpp:315-344).  Particles are loaded on the
+ * host with the reference's Rng (std::mt19937_64 + its uniform and
+ * Box-Muller mappings, proj/include/minipic/rng.hpp:17-51), so the initial
+ * state is bit-identical to SimState::initialize's.  Deck keys that pick CPU
+ * strategies (run.workers, layout, scatter_backend, chunk_size, kernel) are
+ * validated and ignored; run.deterministic / exact_gyration map to the
+ * PIC_* flags.  Hooks are not part of the C surface. */
+typedef struct pic_deck pic_deck;
+typedef struct pic_sim pic_sim;
+/* parse_deck (deck.cpp:200-293): PIC_DECK_PARSE_ERROR names key and line. */
+int pic_deck_parse(const char* text, pic_deck** out);
+int pic_deck_destroy(pic_deck* deck);
+/* apply_override (deck.cpp:361-395), e.g. "species.electron.ppc=4"; a
+ * failed override leaves the deck unchanged. */
+int pic_deck_override(pic_deck* deck, const char* key_eq_value);
+/* serialize_deck (deck.cpp:321-359): canonical text; *len = full length
+ * (the copy into buf is truncated to cap - 1 and NUL-terminated). */
+int pic_deck_serialize(const pic_deck* deck, char* buf, size_t cap, size_t* len);
+/* make_grid (deck.cpp:188-198): spacings from extents, dt resolved. */
+int pic_deck_grid(const pic_deck* deck, pic_grid* out);
+int pic_deck_steps(const pic_deck* deck, long* out);
+/* SimState::initialize on a device. */
+int pic_sim_create(int device, const pic_deck* deck, pic_sim** out);
+int pic_sim_destroy(pic_sim* sim);
+/* The sim's device state as a (borrowed) pic_context: species in deck
+ * order; valid until pic_sim_destroy; do not pic_context_destroy it. */
+int pic_sim_context(pic_sim* sim, pic_context** out);
+/* SimState::step followed by sort_due_species (sim.cpp:217-222). */
+int pic_sim_step(pic_sim* sim);
+int pic_sim_step_count(pic_sim* sim, long* out);
+int pic_sim_refresh_charge_diagnostics(pic_sim* sim);
+/* SimState::emit_diagnostics: the CSV header on first use, then one row. */
+int pic_sim_emit_diagnostics(pic_sim* sim, char* buf, size_t cap, size_t* len);
+/* SimState::run: deck.grid.steps steps with the diagnostic / sort / dump
+ * cadences; CSV to csv_path unless NULL; dumps into run.out_dir. */
+int pic_sim_run(pic_sim* sim, const char* csv_path);
+int pic_sim_dump_fields(pic_sim* sim, const char* path);
+/* SimState::warnings (sim.hpp:171), newline-separated. */
+int pic_sim_warnings(pic_sim* sim, char* buf, size_t cap, size_t* len);
+
 /* ---- timing: CUDA events on the context stream --------------------------*/
 int pic_event_record(pic_context* ctx, int slot); /* slot in [0, 64) */
 int pic_event_elapsed_ms(pic_context* ctx, int a, int b, float* ms);

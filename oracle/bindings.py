@@ -227,6 +227,7 @@ class Ref:
         L.mref_kinetic_energy_centered.argtypes = [G, C.c_float, C.c_float, C.c_long, F32P, I32P, F32P,
                                                    C.POINTER(C.c_float)]
         L.mref_max_abs_lane.argtypes = [G, F32P, C.c_int, C.POINTER(C.c_float)]
+        L.mref_deck_roundtrip.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_long]
         L.mref_sim_new.argtypes = [C.c_char_p]
         L.mref_sim_new.restype = C.c_void_p
         L.mref_sim_free.argtypes = [C.c_void_p]
@@ -303,6 +304,14 @@ class Ref:
         out = C.c_float()
         self._chk(self.lib.mref_max_abs_lane(C.byref(g), f16, lane, C.byref(out)))
         return out.value
+
+    def deck_roundtrip(self, text: str, override: str | None = None) -> str:
+        """serialize_deck(parse_deck(text) [+ apply_override]); raises on
+        parse errors with the reference's message."""
+        buf = C.create_string_buffer(1 << 16)
+        self._chk(self.lib.mref_deck_roundtrip(text.encode(), override.encode() if override else None, buf,
+                                               len(buf)))
+        return buf.value.decode()
 
     def sim(self, deck_text: str) -> "RefSim":
         return RefSim(self, deck_text)

@@ -284,6 +284,18 @@ int mref_max_abs_lane(const mref_grid* g, const float* fields16, int lane,
   });
 }
 
+// ---- deck text (proj/src/deck.cpp) ---------------------------------------
+// parse + serialize; with an override applied when kv != NULL.
+int mref_deck_roundtrip(const char* text, const char* kv, char* buf, long buflen) {
+  return guard([&] {
+    Deck d = parse_deck(text);
+    if (kv) apply_override(d, kv);
+    const std::string t = serialize_deck(d);
+    if (static_cast<long>(t.size()) + 1 > buflen) throw usage_error("deck buffer too small");
+    std::memcpy(buf, t.c_str(), t.size() + 1);
+  });
+}
+
 // ---- SimState (proj/src/sim.cpp) -----------------------------------------
 void* mref_sim_new(const char* deck_text) {
   void* out = nullptr;

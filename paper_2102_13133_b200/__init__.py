@@ -161,6 +161,22 @@ def lib() -> C.CDLL:
         "pic_migrate_counts": [P, C.c_int, C.POINTER(C.c_size_t)],
         "pic_migrate_pack": [P, C.c_int, P, P],
         "pic_migrate_append": [P, C.c_int, P, C.c_size_t],
+        "pic_deck_parse": [C.c_char_p, C.POINTER(P)],
+        "pic_deck_destroy": [P],
+        "pic_deck_override": [P, C.c_char_p],
+        "pic_deck_serialize": [P, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)],
+        "pic_deck_grid": [P, G],
+        "pic_deck_steps": [P, C.POINTER(C.c_long)],
+        "pic_sim_create": [C.c_int, P, C.POINTER(P)],
+        "pic_sim_destroy": [P],
+        "pic_sim_context": [P, C.POINTER(P)],
+        "pic_sim_step": [P],
+        "pic_sim_step_count": [P, C.POINTER(C.c_long)],
+        "pic_sim_refresh_charge_diagnostics": [P],
+        "pic_sim_emit_diagnostics": [P, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)],
+        "pic_sim_run": [P, C.c_char_p],
+        "pic_sim_dump_fields": [P, C.c_char_p],
+        "pic_sim_warnings": [P, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)],
     }
     for name, argtypes in sigs.items():
         fn = getattr(L, name)
@@ -193,13 +209,21 @@ class Context:
     def __init__(self, grid: Grid, device: int = 0):
         self.grid = grid
         self._h = C.c_void_p()
+        self._borrowed = False
         check(lib().pic_context_create(device, C.byref(grid), C.byref(self._h)))
         self.species_names = []
 
+    @classmethod
+    def _borrow(cls, handle: C.c_void_p, grid: Grid, species_names):
+        """A view of a context owned elsewhere (a SimState's)."""
+        ctx = cls.__new__(cls)
+        ctx.grid, ctx._h, ctx._borrowed, ctx.species_names = grid, handle, True, list(species_names)
+        return ctx
+
     def close(self):
-        if self._h:
+        if self._h and not self._borrowed:
             check(lib().pic_context_destroy(self._h))
-            self._h = C.c_void_p()
+        self._h = C.c_void_p()
 
     def __enter__(self):
         return self

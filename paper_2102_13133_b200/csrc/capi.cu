@@ -328,10 +328,6 @@ static void step_host(Context& c, unsigned flags, float* const* lanes7, int32_t*
 // C-ABI
 using namespace picb;
 
-struct pic_context {
-  Context* c;
-};
-
 namespace {
 template <class Fn>
 int guard(Fn&& fn) {
@@ -355,6 +351,11 @@ int guard(Fn&& fn) {
     return PIC_INTERNAL_ERROR;
   }
 }
+}  // namespace
+
+int picb::capi_guard(const std::function<void()>& fn) { return guard(fn); }
+
+namespace {
 Context& C_(pic_context* p) {
   if (!p || !p->c) throw UsageError("null pic_context");
   return *p->c;
@@ -374,13 +375,14 @@ int pic_context_create(int device, const pic_grid* grid, pic_context** out) {
     if (!grid || !out) throw UsageError("pic_context_create: null argument");
     *out = nullptr;
     Context* c = make_context(device, *grid);
-    *out = new pic_context{c};
+    *out = new pic_context{c, false};
   });
 }
 
 int pic_context_destroy(pic_context* ctx) {
   return guard([&] {
     if (!ctx) return;
+    if (ctx->borrowed) throw UsageError("pic_context_destroy: the context belongs to a pic_sim; destroy the sim");
     destroy_context(ctx->c);
     delete ctx;
   });

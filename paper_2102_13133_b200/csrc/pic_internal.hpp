@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -173,4 +174,14 @@ void sort_species(Context& c, Species& s, int order);
 // ---- the step --------------------------------------------------------------
 void step(Context& c, unsigned flags);
 
+// C-ABI error translation (capi.cu): runs fn, maps the exception classes to
+// pic_status codes and records the message for pic_last_error().
+int capi_guard(const std::function<void()>& fn);
+
 }  // namespace picb
+
+// The C-ABI handle: owns its context unless borrowed (a pic_sim's view).
+struct pic_context {
+  picb::Context* c;
+  bool borrowed;
+};
