@@ -451,6 +451,12 @@ class Context:
         fn.argtypes = [C.c_void_p, C.c_int]
         check(fn(self._h, variant))
 
+    def _set_sort_variant(self, variant: int):
+        """Benchmarking hook (not in the public C header): sort strategy."""
+        fn = lib().pic_internal_set_sort_variant
+        fn.argtypes = [C.c_void_p, C.c_int]
+        check(fn(self._h, variant))
+
     def _set_host_chunk(self, particles: int):
         """Testing hook (not in the public C header): pic_step_host chunk size."""
         fn = lib().pic_internal_set_host_chunk

@@ -255,13 +255,17 @@ def test_species_upload_rejects_ghost_ids(pic):
 
 @pytest.mark.parametrize("order", [0, 1])
 @pytest.mark.parametrize("dims,n", [((5, 4, 3), 3000), ((20, 20, 20), 300000), ((2, 2, 2), 1)])
-def test_sort_bitwise(pic, orc, order, dims, n):
+@pytest.mark.parametrize("variant", [0, 1, 2])
+def test_sort_bitwise(pic, orc, order, dims, n, variant):
+    """Every sort strategy (radix with 8- or 9-bit digits, tiled counting
+    sort) gives the reference's stable permutation."""
     g = pic.make_grid(dims)
     rng = np.random.default_rng(21 + order)
     p, ids = rand_particles(g, rng, n, sort=False)
     # skewed occupancy so the interleaved rounds are ragged
     ids[: n // 3] = ids[0]
     with pic.Context(g) as ctx:
+        ctx._set_sort_variant(variant)
         sid = ctx.add_species("s", -1.0, 1.0, n)
         ctx.upload_species(sid, p, ids)
         ctx.sort_particles(sid, order)

@@ -19,14 +19,12 @@ for name, q, m, ppc, uth, drift in cfg["species"]:
     sid = ctx.add_species(name, q, m, ppc * g.interior)
     ctx.load_synthetic(sid, ppc, uth, drift, seed=7)
     sids.append(sid)
-fn = pic.lib().pic_internal_set_sort_variant
-fn.argtypes = [C.c_void_p, C.c_int]
 for rep in range(2):
     for _ in range(stale):
         ctx.step()
     ctx.synchronize()
     for var in variants:
-        pic.check(fn(ctx._h, var))
+        ctx._set_sort_variant(var)
         for s in sids:
             t0 = time.perf_counter()
             ctx.event(0)
