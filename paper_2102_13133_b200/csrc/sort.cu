@@ -102,7 +102,8 @@ __global__ void __launch_bounds__(kThreads)
 radix_hist_kernel(const unsigned* __restrict__ keys, size_t n, int shift, unsigned mask,
                   size_t ntiles, unsigned* __restrict__ table) {
   __shared__ unsigned h[kDigits];
-  for (int d = threadIdx.x; d < kDigits; d += kThreads) h[d] = 0;
+  const int ndig = (int)mask + 1;  // digits of this pass (<= kDigits)
+  for (int d = threadIdx.x; d < ndig; d += kThreads) h[d] = 0;
   __syncthreads();
   const size_t base = (size_t)blockIdx.x * kTile;
   const int lane = threadIdx.x & 31;
@@ -125,14 +126,15 @@ radix_scatter_kernel(const unsigned* __restrict__ keys, const unsigned* __restri
   __shared__ unsigned cnt[kWarps][kDigits];
   __shared__ unsigned base_d[kDigits];
   __shared__ unsigned goff[kDigits];
-  for (int d = threadIdx.x; d < kDigits; d += kThreads) {
+  const int ndig = (int)mask + 1;  // digits of this pass (<= kDigits)
+  for (int d = threadIdx.x; d < ndig; d += kThreads) {
     base_d[d] = 0;
-    goff[d] = d <= (int)mask ? offsets[(size_t)d * ntiles + blockIdx.x] : 0u;
+    goff[d] = offsets[(size_t)d * ntiles + blockIdx.x];
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const size_t tbase = (size_t)blockIdx.x * kTile;
   for (int r = 0; r < kItems; ++r) {
-    for (int d = threadIdx.x; d < kDigits; d += kThreads)
+    for (int d = threadIdx.x; d < ndig; d += kThreads)
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) cnt[w][d] = 0;
     __syncthreads();
@@ -145,7 +147,7 @@ radix_scatter_kernel(const unsigned* __restrict__ keys, const unsigned* __restri
     const unsigned rank = __popc(peers & lanemask_lt());
     if (valid && rank == 0) cnt[warp][d] = __popc(peers);
     __syncthreads();
-    for (int dd = threadIdx.x; dd < kDigits; dd += kThreads) {
+    for (int dd = threadIdx.x; dd < ndig; dd += kThreads) {
       unsigned run = base_d[dd];
 #pragma unroll
       for (int w = 0; w < kWarps; ++w) {
