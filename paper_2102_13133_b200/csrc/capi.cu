@@ -155,7 +155,7 @@ Context* make_context(int device, const pic_grid& g) {
     CUDA_OK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CUDA_OK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     if (const char* v = std::getenv("PIC_PUSH_VARIANT")) c->push_variant = std::atoi(v);  // profiling knob
-    if (const char* v = std::getenv("PIC_SORT_VARIANT")) c->sort_variant = std::atoi(v);  // profiling knob
+    if (const char* v = std::getenv("PIC_SORT_VARIANT")) set_sort_variant(*c, std::atoi(v));  // profiling knob
     const size_t V = (size_t)gc.V;
     CUDA_OK(cudaMalloc(&c->f, F_COUNT * V * sizeof(float)));
     CUDA_OK(cudaMalloc(&c->interp, kInterpF4 * V * sizeof(float4)));
@@ -850,14 +850,9 @@ int pic_phase_timings(pic_context* ctx, double out_ms[5], int reset) {
   });
 }
 
-// Not in the public header: sort strategy (benchmarking): 0 = radix with
-// 8-bit digits (default), 1 = tiled counting sort, 2 = radix, 9-bit digits.
+// Not in the public header: sort strategy (benchmarking).
 int pic_internal_set_sort_variant(pic_context* ctx, int variant) {
-  return guard([&] {
-    Context& c = C_(ctx);
-    c.sort_variant = variant == 1 ? 1 : 0;
-    c.sort_radix_bits = variant == 2 ? 9 : 8;
-  });
+  return guard([&] { set_sort_variant(C_(ctx), variant); });
 }
 // Not in the public header: selects an advance_p strategy (benchmarking).
 int pic_internal_set_push_variant(pic_context* ctx, int variant) {

@@ -255,10 +255,11 @@ def test_species_upload_rejects_ghost_ids(pic):
 
 @pytest.mark.parametrize("order", [0, 1])
 @pytest.mark.parametrize("dims,n", [((5, 4, 3), 3000), ((20, 20, 20), 300000), ((2, 2, 2), 1)])
-@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3, 4])
 def test_sort_bitwise(pic, orc, order, dims, n, variant):
-    """Every sort strategy (radix with 8- or 9-bit digits, tiled counting
-    sort) gives the reference's stable permutation."""
+    """Every sort strategy (radix with 9- or 8-bit digits, ballot or
+    match.any digit grouping; tiled counting sort) gives the reference's
+    stable permutation."""
     g = pic.make_grid(dims)
     rng = np.random.default_rng(21 + order)
     p, ids = rand_particles(g, rng, n, sort=False)
