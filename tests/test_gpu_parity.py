@@ -144,7 +144,7 @@ def test_advance_p_parity(pic, orc, dims, n, u, deterministic):
     assert (wids != _push_case.ids0).mean() > 0.02
 
 
-PUSH_VARIANTS = list(range(37))
+PUSH_VARIANTS = list(range(43))
 
 
 @pytest.mark.parametrize("variant", PUSH_VARIANTS)
@@ -159,7 +159,7 @@ def test_advance_p_strategies(pic, orc, variant):
     assert_close(gacc, wacc, ACC_RTOL, what="accumulator")
 
 
-@pytest.mark.parametrize("variant", [0, 7, 10, 13, 18, 20, 21, 30, 31, 33, 35, 36])
+@pytest.mark.parametrize("variant", [0, 7, 10, 13, 18, 20, 21, 30, 31, 33, 35, 36, 39, 40, 41])
 @pytest.mark.parametrize("dims,n,u,sort", [((40, 6, 5), 240000, 0.4, True), ((7, 6, 5), 30000, 1.2, False),
                                            ((4, 3, 2), 31, 0.5, True)])
 def test_advance_p_strategies_layouts(pic, orc, variant, dims, n, u, sort):
