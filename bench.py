@@ -65,6 +65,19 @@ CONFIGS = {
                           ("ion", 0.125, 12.5, 32, 0.01, (0.0, 0.0, 0.0))]),
 }
 
+def _harris_config():
+    """configs[2]: double Harris sheet (paper_2102_13133_b200/decks.py), 256 x 64
+    x 256 cells, four species (sheet / background electrons and ions) of 64
+    ppc each: 1.07e9 particles per GPU; built through the API (the
+    reference's deck text cannot express it)."""
+    from paper_2102_13133_b200.decks import Harris
+    d = Harris(n=(256, 64, 256), ppc=64)
+    return dict(n=256, h=d.h, dt=d.dt, sort_interval=20, deck=d,
+                species=[(name, q, m, d.ppc, uth, drift) for name, q, m, uth, drift, _ in d.species()])
+
+
+CONFIGS["harris"] = _harris_config()
+
 BYTES_PER_PUSH = 64  # 32 B record read + 32 B record written (SURVEY §8d)
 
 
@@ -194,14 +207,18 @@ def run_ours(args, rank, world):
 
     cfg = CONFIGS[args.config]
     n = cfg["n"]
-    g = pic.make_grid(n, cfg["h"], dt=cfg["dt"])
+    deck = cfg.get("deck")
+    g = deck.grid() if deck else pic.make_grid(n, cfg["h"], dt=cfg["dt"])
     ctx = pic.Context(g, device=args.device)
     sids = []
-    for si, (name, q, m, ppc, uth, drift) in enumerate(cfg["species"]):
-        cap = ppc * g.interior
-        sid = ctx.add_species(name, q, m, cap)
-        ctx.load_synthetic(sid, ppc, uth, drift, seed=1234 + 7919 * rank)
-        sids.append(sid)
+    if deck:
+        sids = deck.load(ctx, seed=1234 + 7919 * rank)
+    else:
+        for si, (name, q, m, ppc, uth, drift) in enumerate(cfg["species"]):
+            cap = ppc * g.interior
+            sid = ctx.add_species(name, q, m, cap)
+            ctx.load_synthetic(sid, ppc, uth, drift, seed=1234 + 7919 * rank)
+            sids.append(sid)
     ctx.synchronize()
     npart = sum(ctx.species_count(s) for s in sids)
     sort_interval = cfg["sort_interval"]
@@ -285,16 +302,29 @@ def run_ours_decomposed(args, rank, world):
     torch.cuda.set_device(args.device)
     cfg = CONFIGS[args.config]
     n = cfg["n"]
-    geom = SlabGeometry(n * world, n, n, world, h=(cfg["h"],) * 3, dt=cfg["dt"])
+    deck = cfg.get("deck")
+    if deck:  # weak scaling: the global box grows in x, (nx N) x ny x nz
+        import dataclasses
+        deck = dataclasses.replace(deck, n=(deck.n[0] * world, deck.n[1], deck.n[2]))
+        geom = SlabGeometry(*deck.n, world, h=(cfg["h"],) * 3, dt=cfg["dt"])
+    else:
+        geom = SlabGeometry(n * world, n, n, world, h=(cfg["h"],) * 3, dt=cfg["dt"])
     slab = CudaSlab(geom.local_grid(), rank, rank == 0, device=args.device)
     sim = DecomposedSim(geom, {rank: slab}, DistTransport(rank, world))
     ctx = slab.ctx
     g = geom.local_grid()
     sids = []
-    for name, q, m, ppc, uth, drift in cfg["species"]:
-        sid = sim.add_species(name, q, m, int(ppc * g.interior * 1.02) + 65536)
-        ctx.load_synthetic(sid, ppc, uth, drift, seed=1234 + 7919 * rank)
-        sids.append(sid)
+    if deck:
+        for name, q, m, uth, drift, sheet in deck.species():
+            sid = sim.add_species(name, q, m, int(deck.ppc * g.interior * 1.02) + 65536)
+            ctx.load_harris(sid, deck.ppc, uth, drift, seed=1234 + 7919 * rank, **sheet)
+            sids.append(sid)
+        ctx.upload_fields(deck.fields(g, x0=geom.x0(rank)))
+    else:
+        for name, q, m, ppc, uth, drift in cfg["species"]:
+            sid = sim.add_species(name, q, m, int(ppc * g.interior * 1.02) + 65536)
+            ctx.load_synthetic(sid, ppc, uth, drift, seed=1234 + 7919 * rank)
+            sids.append(sid)
     ctx.synchronize()
     sort_interval = cfg["sort_interval"]
     step_count = [0]
@@ -467,6 +497,10 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
+        if cfg.get("deck"):
+            print(json.dumps({"impl": "reference", "unavailable": f"the reference's deck text cannot express the "
+                              f"{args.config} deck (built through the API here)"}))
+            return
         r = cpu_reference(args.config, max(1, min(args.steps, 3)), max(1, min(args.warmup, 1)),
                           sample_n=args.cpu_sample_n)
         if r is None:
@@ -509,7 +543,9 @@ def main():
     achieved = res["npart"] / res["nspecies"] * BYTES_PER_PUSH / (res["push_ms_per_launch"] / 1e3) / 1e9
     prof = profile_traffic()
     cpu = None
-    if not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only
+    if not args.no_cpu_baseline and world == 1 and cfg.get("deck"):
+        cpu = {"value": None, "note": "the reference cannot express this deck; see --config two_stream"}
+    elif not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only
         try:
             r = cpu_reference(args.config, 3, 1, sample_n=args.cpu_sample_n)
             if r:
@@ -530,7 +566,8 @@ def main():
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f32",
-        "data": "synthetic (device counter-RNG load: uniform offsets, drifting Maxwellian momenta)",
+        "data": "synthetic (device counter-RNG load: uniform offsets, drifting Maxwellian momenta"
+                + (", sech^2 Harris weights, A_y fields)" if cfg.get("deck") else ")"),
         "config": {"workload": args.config, "cells": f"{gl.nx}x{gl.ny}x{gl.nz}", "particles_per_gpu": res["npart"],
                    "ppc": sum(s[3] for s in cfg["species"]), "dt": g.dt, "sort_interval": cfg["sort_interval"],
                    "parallelism": f"x-slab decomposition over {world} GPUs (NCCL halo + migration)"

@@ -105,6 +105,22 @@ int pic_species_load_synthetic(pic_context* ctx, int species, int ppc,
                                float u_th, const float drift[3],
                                uint64_t seed);
 
+/* Double Harris current sheet (BASELINE configs[2]; built through the API,
+ * as SURVEY §8d C3 notes the reference cannot express it as deck text): the
+ * synthetic load with particle weights w(z) = background + amplitude *
+ * (sech^2((z - z1)/L) + sech^2((z - z2)/L)), z = (iz - 1 + (oz + 1)/2) hz,
+ * and, with flip_drift, the drift reversed for particles nearer z2 (the two
+ * sheets carry opposite currents).  Fields (B_x = B0 tanh profile) are
+ * uploaded by the caller (paper_2102_13133_b200/decks.py). */
+typedef struct pic_sheet {
+  float z1, z2, half_width;
+  float background, amplitude;
+  int flip_drift;
+} pic_sheet;
+int pic_species_load_harris(pic_context* ctx, int species, int ppc,
+                            float u_th, const float drift[3], uint64_t seed,
+                            const pic_sheet* sheet);
+
 /* ---- fields: FieldArray (proj/include/minipic/fields.hpp:21-38) --------- */
 int pic_fields_upload(pic_context* ctx, const float* fields16);
 int pic_fields_download(pic_context* ctx, float* fields16);

@@ -94,6 +94,13 @@ class Diag(C.Structure):
 _lib = None
 
 
+class Sheet(C.Structure):
+    """pic_sheet (include/pic_b200.h)."""
+
+    _fields_ = [("z1", C.c_float), ("z2", C.c_float), ("half_width", C.c_float),
+                ("background", C.c_float), ("amplitude", C.c_float), ("flip_drift", C.c_int)]
+
+
 def lib() -> C.CDLL:
     """Loads libpic_b200.so (fails loudly if it has not been built)."""
     global _lib
@@ -121,6 +128,7 @@ def lib() -> C.CDLL:
         "pic_species_upload_records": [P, C.c_int, C.c_size_t, P, P],
         "pic_species_download_records": [P, C.c_int, P, P],
         "pic_species_load_synthetic": [P, C.c_int, C.c_int, C.c_float, F32, C.c_uint64],
+        "pic_species_load_harris": [P, C.c_int, C.c_int, C.c_float, F32, C.c_uint64, C.POINTER(Sheet)],
         "pic_fields_upload": [P, F32],
         "pic_fields_download": [P, F32],
         "pic_interpolators_download": [P, F32],
@@ -279,6 +287,14 @@ class Context:
 
     def load_synthetic(self, sid: int, ppc: int, u_th: float, drift=(0.0, 0.0, 0.0), seed: int = 1):
         check(lib().pic_species_load_synthetic(self._h, sid, ppc, u_th, np.asarray(drift, np.float32), seed))
+
+    def load_harris(self, sid: int, ppc: int, u_th: float, drift=(0.0, 0.0, 0.0), seed: int = 1, *,
+                    z1: float, z2: float, half_width: float, background: float = 0.0,
+                    amplitude: float = 1.0, flip_drift: bool = True):
+        """Synthetic load with double-Harris-sheet weights (pic_species_load_harris)."""
+        sh = Sheet(z1, z2, half_width, background, amplitude, int(flip_drift))
+        check(lib().pic_species_load_harris(self._h, sid, ppc, u_th, np.asarray(drift, np.float32), seed,
+                                            C.byref(sh)))
 
     # --- fields ------------------------------------------------------------
     def upload_fields(self, f16: np.ndarray):

@@ -512,7 +512,20 @@ int pic_species_load_synthetic(pic_context* ctx, int species, int ppc, float u_t
     if (ppc < 0) throw UsageError("load_synthetic: ppc must be >= 0");
     const float zero[3] = {0, 0, 0};
     launch_load_synthetic(c, species_at(c, species), ppc, u_th, drift ? drift : zero,
-                          seed + 0x9e3779b9ULL * (uint64_t)(species + 1));
+                          seed + 0x9e3779b9ULL * (uint64_t)(species + 1), nullptr);
+    check_launch();
+  });
+}
+
+int pic_species_load_harris(pic_context* ctx, int species, int ppc, float u_th, const float drift[3],
+                            uint64_t seed, const pic_sheet* sheet) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    if (ppc < 0) throw UsageError("load_harris: ppc must be >= 0");
+    if (!sheet) throw UsageError("load_harris: sheet is null");
+    const float zero[3] = {0, 0, 0};
+    launch_load_synthetic(c, species_at(c, species), ppc, u_th, drift ? drift : zero,
+                          seed + 0x9e3779b9ULL * (uint64_t)(species + 1), sheet);
     check_launch();
   });
 }

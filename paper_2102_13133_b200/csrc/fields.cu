@@ -313,9 +313,18 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 __device__ __forceinline__ float u01(uint64_t h) {  // [0, 1)
   return (float)(h >> 40) * (1.0f / 16777216.0f);
 }
+// Density profile of a synthetic load (uniform: bg 1, amp 0): particle
+// weight w(z) = bg + amp (sech^2((z - z1) / L) + sech^2((z - z2) / L)), and
+// with flip the drift changes sign for particles nearer z2 than z1 (the
+// counter-propagating currents of a double Harris sheet).  z is the physical
+// coordinate of the particle, (iz - 1 + (oz + 1) / 2) hz.
+struct Sheet {
+  float bg, amp, z1, z2, L, hz;
+  int flip;
+};
 __global__ void load_synthetic_kernel(GridC g, int ppc, float u_th, float dx0, float dy0, float dz0,
                                       uint64_t seed, size_t n, float4* __restrict__ pos,
-                                      float4* __restrict__ mom) {
+                                      float4* __restrict__ mom, Sheet sh) {
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const long long cell = (long long)(i / (size_t)ppc);
@@ -334,8 +343,15 @@ __global__ void load_synthetic_kernel(GridC g, int ppc, float u_th, float dx0, f
     nrm[2 * k] = r * cospif(2.0f * b);
     nrm[2 * k + 1] = r * sinpif(2.0f * b);
   }
+  float w = 1.0f, sgn = 1.0f;
+  if (sh.amp != 0.0f || sh.bg != 1.0f) {
+    const float zp = ((float)(iz - 1) + 0.5f * (z + 1.0f)) * sh.hz;
+    const float c1 = coshf((zp - sh.z1) / sh.L), c2 = coshf((zp - sh.z2) / sh.L);
+    w = sh.bg + sh.amp * (1.0f / (c1 * c1) + 1.0f / (c2 * c2));
+    if (sh.flip && fabsf(zp - sh.z2) < fabsf(zp - sh.z1)) sgn = -1.0f;
+  }
   pos[i] = make_float4(x, y, z, __int_as_float(voxel_of(g, ix, iy, iz)));
-  mom[i] = make_float4(dx0 + u_th * nrm[0], dy0 + u_th * nrm[1], dz0 + u_th * nrm[2], 1.0f);
+  mom[i] = make_float4(sgn * dx0 + u_th * nrm[0], sgn * dy0 + u_th * nrm[1], sgn * dz0 + u_th * nrm[2], w);
 }
 
 }  // namespace
@@ -423,13 +439,21 @@ void launch_unpack_species(Context& c, Species& s, float* l7, int32_t* ids) {
 }
 
 void launch_load_synthetic(Context& c, Species& s, int ppc, float u_th, const float drift[3],
-                           uint64_t seed) {
+                           uint64_t seed, const pic_sheet* sheet) {
   const size_t n = (size_t)ppc * (size_t)c.gc.nx * c.gc.ny * c.gc.nz;
   if (n > s.cap) throw UsageError("load_synthetic: ppc * interior voxels exceeds species capacity");
+  Sheet sh{1.0f, 0.0f, 0.0f, 0.0f, 1.0f, c.grid.hz, 0};
+  if (sheet) {
+    if (!(sheet->half_width > 0.0f)) throw UsageError("load_harris: half_width must be > 0");
+    if (sheet->background < 0.0f || sheet->amplitude < 0.0f)
+      throw UsageError("load_harris: background and amplitude must be >= 0");
+    sh = Sheet{sheet->background, sheet->amplitude, sheet->z1, sheet->z2, sheet->half_width, c.grid.hz,
+               sheet->flip_drift ? 1 : 0};
+  }
   s.n = n;
   if (n == 0) return;
   load_synthetic_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(
-      c.gc, ppc, u_th, drift[0], drift[1], drift[2], seed, n, s.pos, s.mom);
+      c.gc, ppc, u_th, drift[0], drift[1], drift[2], seed, n, s.pos, s.mom, sh);
   c.count_launch();
 }
 

@@ -135,7 +135,7 @@ void launch_pack_species(Context& c, Species& s, const float* lanes7_dev, const 
                          size_t n);
 void launch_unpack_species(Context& c, Species& s, float* lanes7_dev, int32_t* ids_dev);
 void launch_load_synthetic(Context& c, Species& s, int ppc, float u_th, const float drift[3],
-                           uint64_t seed);
+                           uint64_t seed, const pic_sheet* sheet);
 void launch_interp_to_lanes(Context& c, float* out18);
 void launch_lanes_to_interp(Context& c, const float* in18);
 
