@@ -179,6 +179,59 @@ int pic_step_host(pic_context* ctx, unsigned flags, float* const* lanes7,
  * Slabs must have equal nx.  pic_step / pic_step_host refuse an x-open
  * context: the host sequences the step around the exchanges. */
 int pic_set_x_open(pic_context* ctx, int x_open, int low_wraps);
+
+/* ---- non-periodic x boundaries (NOT IN REFERENCE: the
+ * reference is periodic only, so these are designed fresh and checked by
+ * self-consistency tests, tests/test_gpu_boundaries.py) ------------------
+ * side 0 = low x face (x = 0), 1 = high x face (x = nx hx).  A wall side
+ * replaces the periodic wrap / fold / ghost copy on that face:
+ *   particles  PIC_PBC_ABSORB   leave the domain: removed after the push
+ *                               (store compacted in index order), the part
+ *                               of their last segment beyond the wall is
+ *                               not deposited;
+ *              PIC_PBC_REFLECT  specular: mirrored back into the boundary
+ *                               cell (x offset -> -x offset, u_x -> -u_x),
+ *                               the current beyond the wall folded back as
+ *                               its mirror image (charge-conserving);
+ *   fields     PIC_FBC_PEC      conductor: tangential E = 0 on the wall;
+ *              PIC_FBC_MUR      first-order Mur absorbing condition on the
+ *                               tangential E at the wall (normal incidence).
+ * Both sides must be periodic or both walls; not with decomposition
+ * (pic_set_x_open).  Push variants 0 (deterministic), 42 and 43. */
+#define PIC_PBC_PERIODIC 0
+#define PIC_PBC_ABSORB 1
+#define PIC_PBC_REFLECT 2
+#define PIC_FBC_PERIODIC 0
+#define PIC_FBC_PEC 1
+#define PIC_FBC_MUR 2
+int pic_set_x_boundary(pic_context* ctx, int side, int particle_bc, int field_bc);
+/* particles absorbed through the low / high x wall since the last call
+ * (synchronises) */
+int pic_absorbed_counts(pic_context* ctx, uint64_t out[2], int reset);
+
+/* Laser: a soft source on the node plane x = (ix - 1) hx — after every E
+ * update E_pol += dt (2 e0 / hx) s(t) g(y, z) on that plane (a current sheet
+ * radiating amplitude ~e0 each way), s(t) = sin(omega t) ramped in over
+ * ramp_steps steps (sin^2), g = exp(-((y - y0)^2 + (z - z0)^2) / waist^2)
+ * (waist <= 0: plane wave).  pol 1 = E_y, 2 = E_z.  e0 = 0 removes it. */
+typedef struct pic_laser {
+  int ix, pol;
+  float e0, omega, ramp_steps, y0, z0, waist;
+} pic_laser;
+int pic_set_laser(pic_context* ctx, const pic_laser* laser);
+
+/* Emitter hook: after every push, per_cell new particles of `species` are
+ * injected into each boundary cell of x side `side` (uniform offsets,
+ * Maxwellian u_th momenta, drift[0] directed into the domain).  Injected
+ * particles deposit no current in their first step (they appear, as in a
+ * loader).  per_cell = 0 removes the species' emitter on that side. */
+int pic_set_emitter(pic_context* ctx, int species, int side, int per_cell, float u_th,
+                    const float drift[3], uint64_t seed);
+
+/* Synthetic load restricted to the cells with x index in [ix_lo, ix_hi]
+ * (a plasma slab, e.g. the LPI deck's target). */
+int pic_species_load_slab(pic_context* ctx, int species, int ppc, float u_th,
+                          const float drift[3], uint64_t seed, int ix_lo, int ix_hi);
 /* Runs the context's work on a caller-provided cudaStream_t (a created
  * stream, e.g. torch's current stream, so NCCL send/recv order with the
  * kernels); NULL restores the context's own stream (the legacy default

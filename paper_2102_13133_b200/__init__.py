@@ -94,6 +94,17 @@ class Diag(C.Structure):
 _lib = None
 
 
+class Laser(C.Structure):
+    """pic_laser (include/pic_b200.h)."""
+
+    _fields_ = [("ix", C.c_int), ("pol", C.c_int), ("e0", C.c_float), ("omega", C.c_float),
+                ("ramp_steps", C.c_float), ("y0", C.c_float), ("z0", C.c_float), ("waist", C.c_float)]
+
+
+PBC_PERIODIC, PBC_ABSORB, PBC_REFLECT = 0, 1, 2
+FBC_PERIODIC, FBC_PEC, FBC_MUR = 0, 1, 2
+
+
 class Sheet(C.Structure):
     """pic_sheet (include/pic_b200.h)."""
 
@@ -129,6 +140,11 @@ def lib() -> C.CDLL:
         "pic_species_download_records": [P, C.c_int, P, P],
         "pic_species_load_synthetic": [P, C.c_int, C.c_int, C.c_float, F32, C.c_uint64],
         "pic_species_load_harris": [P, C.c_int, C.c_int, C.c_float, F32, C.c_uint64, C.POINTER(Sheet)],
+        "pic_species_load_slab": [P, C.c_int, C.c_int, C.c_float, F32, C.c_uint64, C.c_int, C.c_int],
+        "pic_set_x_boundary": [P, C.c_int, C.c_int, C.c_int],
+        "pic_absorbed_counts": [P, C.POINTER(C.c_uint64), C.c_int],
+        "pic_set_laser": [P, C.POINTER(Laser)],
+        "pic_set_emitter": [P, C.c_int, C.c_int, C.c_int, C.c_float, F32, C.c_uint64],
         "pic_fields_upload": [P, F32],
         "pic_fields_download": [P, F32],
         "pic_interpolators_download": [P, F32],
@@ -295,6 +311,28 @@ class Context:
         sh = Sheet(z1, z2, half_width, background, amplitude, int(flip_drift))
         check(lib().pic_species_load_harris(self._h, sid, ppc, u_th, np.asarray(drift, np.float32), seed,
                                             C.byref(sh)))
+
+    def load_slab(self, sid: int, ppc: int, u_th: float, drift=(0.0, 0.0, 0.0), seed: int = 1, *,
+                  ix_lo: int, ix_hi: int):
+        """Synthetic load of the cells with x index in [ix_lo, ix_hi] (pic_species_load_slab)."""
+        check(lib().pic_species_load_slab(self._h, sid, ppc, u_th, np.asarray(drift, np.float32), seed,
+                                          ix_lo, ix_hi))
+
+    # --- non-periodic x boundaries, laser, emitter (pic_set_x_boundary ...) ---
+    def set_x_boundary(self, side: int, particle_bc: int, field_bc: int):
+        check(lib().pic_set_x_boundary(self._h, side, particle_bc, field_bc))
+
+    def absorbed_counts(self, reset: bool = False):
+        out = (C.c_uint64 * 2)()
+        check(lib().pic_absorbed_counts(self._h, out, int(reset)))
+        return int(out[0]), int(out[1])
+
+    def set_laser(self, ix: int, e0: float, omega: float, pol: int = 1, ramp_steps: float = 0.0,
+                  y0: float = 0.0, z0: float = 0.0, waist: float = 0.0):
+        check(lib().pic_set_laser(self._h, C.byref(Laser(ix, pol, e0, omega, ramp_steps, y0, z0, waist))))
+
+    def set_emitter(self, sid: int, side: int, per_cell: int, u_th: float, drift=(0.0, 0.0, 0.0), seed: int = 1):
+        check(lib().pic_set_emitter(self._h, sid, side, per_cell, u_th, np.asarray(drift, np.float32), seed))
 
     # --- fields ------------------------------------------------------------
     def upload_fields(self, f16: np.ndarray):

@@ -218,23 +218,37 @@ static void step_prologue(Context& c) {
   c.phase_end();
 }
 
+// With x walls (boundary.cu) the x face work changes: wall fold of the
+// accumulator's x ghost planes before the y / z folds, the wall-plane B_x
+// after each B half step, Mur's saved planes, the laser source and the wall
+// E condition around the E update.
 static void step_epilogue(Context& c) {
+  const bool walls = has_walls(c);
   c.phase_begin(Context::kPhScatter);
+  if (walls) launch_wall_fold(c);
   launch_ghost_fold(c);
   c.phase_end();
   c.phase_begin(Context::kPhField);
   launch_advance_b(c, 0.5f);
+  if (walls) launch_wall_b(c, 0.5f);
   launch_ghost_sync(c);
+  if (walls) launch_wall_e_save(c);
   launch_unload_advance_e(c, true, true);
+  launch_laser(c);
+  if (walls) launch_wall_e(c);
   launch_ghost_sync(c);
   launch_advance_b(c, 0.5f);
+  if (walls) launch_wall_b(c, 0.5f);
   launch_ghost_sync(c);
   c.phase_end();
+  ++c.steps_done;
 }
 
 void step(Context& c, unsigned flags) {
   const bool det = (flags & PIC_DETERMINISTIC) != 0;
   const bool exact = (flags & PIC_EXACT_GYRATION) != 0;
+  const bool walls = has_walls(c);
+  check_walls(c, det);
   step_prologue(c);
   c.phase_begin(Context::kPhPush);
   for (auto& s : c.species) {
@@ -242,7 +256,9 @@ void step(Context& c, unsigned flags) {
       launch_advance_p_deterministic(c, s, exact);
     else
       launch_advance_p(c, s, exact);
+    if (walls && (c.gc.wall_p[0] == PIC_PBC_ABSORB || c.gc.wall_p[1] == PIC_PBC_ABSORB)) absorb_compact(c, s);
   }
+  if (!c.emitters.empty()) run_emitters(c);
   c.phase_end();
   step_epilogue(c);
 }
@@ -664,7 +680,8 @@ int pic_sort_particles(pic_context* ctx, int species, int order) {
 }
 int pic_step(pic_context* ctx, unsigned flags) {
   return guard([&] {
-    if (C_(ctx).gc.xopen) throw UsageError("pic_step: x-open (decomposed) context; the host sequences the step");
+    if (C_(ctx).gc.xopen && !has_walls(C_(ctx)))
+      throw UsageError("pic_step: x-open (decomposed) context; the host sequences the step");
     step(C_(ctx), flags);
     check_launch();
   });
@@ -673,7 +690,7 @@ int pic_step(pic_context* ctx, unsigned flags) {
 int pic_step_host(pic_context* ctx, unsigned flags, float* const* lanes7, int32_t* const* ids) {
   return guard([&] {
     Context& c = C_(ctx);
-    if (c.gc.xopen) throw UsageError("pic_step_host: x-open (decomposed) context");
+    if (c.gc.xopen) throw UsageError("pic_step_host: x-open (decomposed) or walled context");
     if (flags & PIC_DETERMINISTIC) {
       // ordered replay needs whole-species passes: upload, step, download
       for (size_t s = 0; s < c.species.size(); ++s) {
@@ -700,6 +717,63 @@ int pic_step_host(pic_context* ctx, unsigned flags, float* const* lanes7, int32_
     }
     check_launch();
     quiesce(c);
+  });
+}
+
+int pic_set_x_boundary(pic_context* ctx, int side, int particle_bc, int field_bc) {
+  return guard([&] { set_x_boundary(C_(ctx), side, particle_bc, field_bc); });
+}
+
+int pic_absorbed_counts(pic_context* ctx, uint64_t out[2], int reset) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    if (!out) throw UsageError("absorbed_counts: out is null");
+    CUDA_OK(cudaStreamSynchronize(c.stream));
+    out[0] = c.absorbed[0];
+    out[1] = c.absorbed[1];
+    if (reset) c.absorbed[0] = c.absorbed[1] = 0;
+  });
+}
+
+int pic_set_laser(pic_context* ctx, const pic_laser* laser) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    if (!laser) throw UsageError("laser: null");
+    if (laser->e0 != 0.f) {
+      if (laser->ix < 1 || laser->ix > c.gc.nx) throw UsageError("laser: plane ix outside [1, nx]");
+      if (laser->pol != 1 && laser->pol != 2) throw UsageError("laser: pol must be 1 (E_y) or 2 (E_z)");
+    }
+    c.laser = *laser;
+  });
+}
+
+int pic_set_emitter(pic_context* ctx, int species, int side, int per_cell, float u_th, const float drift[3],
+                    uint64_t seed) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    species_at(c, species);
+    if (side != 0 && side != 1) throw UsageError("emitter: side must be 0 or 1");
+    if (per_cell < 0) throw UsageError("emitter: per_cell must be >= 0");
+    auto& E = c.emitters;
+    E.erase(std::remove_if(E.begin(), E.end(),
+                           [&](const Context::Emitter& e) { return e.species == species && e.side == side; }),
+            E.end());
+    if (per_cell > 0) {
+      Context::Emitter e{species, side, per_cell, u_th, {0.f, 0.f, 0.f}, seed};
+      if (drift) std::copy(drift, drift + 3, e.drift);
+      E.push_back(e);
+    }
+  });
+}
+
+int pic_species_load_slab(pic_context* ctx, int species, int ppc, float u_th, const float drift[3], uint64_t seed,
+                          int ix_lo, int ix_hi) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    const float zero[3] = {0, 0, 0};
+    load_slab(c, species_at(c, species), ppc, u_th, drift ? drift : zero,
+              seed + 0x9e3779b9ULL * (uint64_t)(species + 1), ix_lo, ix_hi);
+    check_launch();
   });
 }
 

@@ -148,6 +148,7 @@ void ensure_mig_lists(Context& c, Species& s) {
 }
 
 void set_x_open(Context& c, bool open, bool low_wraps) {
+  if (has_walls(c)) throw UsageError("x-open: the context has x walls (pic_set_x_boundary)");
   c.gc.xopen = open ? 1 : 0;
   c.gc.x_low_wraps = low_wraps ? 1 : 0;
   if (open)
@@ -244,9 +245,10 @@ void migrate_pack(Context& c, Species& s, void* low_dst, void* high_dst) {
   CUDA_OK(cudaMemcpyAsync(raw + nl, s.mig_idx + s.mig_cap, (size_t)nh * 4, cudaMemcpyDeviceToDevice, c.stream));
   tmp_bytes = need;
   CUDA_OK(cub::DeviceRadixSort::SortKeys(tmp, tmp_bytes, raw, all, (int)E, 0, 32, c.stream));
-  mig_pack_kernel<<<(E + 255) / 256, 256, 0, c.stream>>>(c.gc, e, nl, nh, s.pos, s.mom,
-                                                         static_cast<float4*>(low_dst),
-                                                         static_cast<float4*>(high_dst));
+  if (low_dst || high_dst)  // absorbing walls discard (boundary.cu)
+    mig_pack_kernel<<<(E + 255) / 256, 256, 0, c.stream>>>(c.gc, e, nl, nh, s.pos, s.mom,
+                                                           static_cast<float4*>(low_dst),
+                                                           static_cast<float4*>(high_dst));
   // holes below n' = n - E: the emigrants with index < n' (a prefix of all[])
   const unsigned long long nnew = (unsigned long long)s.n - E;
   std::vector<unsigned> h_all(E);

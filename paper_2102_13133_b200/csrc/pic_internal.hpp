@@ -78,12 +78,24 @@ struct Context {
   int sort_radix_bits = 9;  // LSD digit width (passes = ceil(key bits / width), widths evened out)
   int sort_match = 1;       // group equal digits with match.any (0: per-bit ballots)
   int num_sms = 148;
+  // non-periodic x boundaries (boundary.cu): absorbed particle counts per
+  // side, the laser source, emitter hooks, steps taken (laser clock)
+  uint64_t absorbed[2] = {0, 0};
+  pic_laser laser{};
+  struct Emitter {
+    int species, side, per_cell;
+    float u_th, drift[3];
+    uint64_t seed;
+  };
+  std::vector<Emitter> emitters;
+  long long steps_done = 0;
   cudaEvent_t events[64] = {};
 
   enum ScratchSlot {
     kScrStage = 0, kScrNseg, kScrOff, kScrSegKey, kScrSegW,
     kScrKeyA, kScrValA, kScrKeyB, kScrValB, kScrHist, kScrScan,
-    kScrCount, kScrStart, kScrWithin, kScrStaging, kScrSmall, kScrDiag, kScrMigA, kScrMigB, kScrMigC, kScrMigT, kScrN
+    kScrCount, kScrStart, kScrWithin, kScrStaging, kScrSmall, kScrDiag, kScrMigA, kScrMigB, kScrMigC, kScrMigT,
+    kScrWall, kScrN
   };
   void* scratch[kScrN] = {};
   size_t scratch_size[kScrN] = {};
@@ -141,6 +153,18 @@ void launch_lanes_to_interp(Context& c, const float* in18);
 
 // ---- domain decomposition in x (domain.cu) -----------------------
 void ensure_mig_lists(Context& c, Species& s);
+// boundary.cu
+bool has_walls(const Context& c);
+void set_x_boundary(Context& c, int side, int pbc, int fbc);
+void check_walls(const Context& c, bool deterministic);
+void absorb_compact(Context& c, Species& s);
+void launch_wall_fold(Context& c);
+void launch_wall_e_save(Context& c);
+void launch_wall_e(Context& c);
+void launch_wall_b(Context& c, float frac);
+void launch_laser(Context& c);
+void run_emitters(Context& c);
+void load_slab(Context& c, Species& s, int ppc, float u_th, const float drift[3], uint64_t seed, int lo, int hi);
 void set_x_open(Context& c, bool open, bool low_wraps);
 // halo planes: kind 0 = accumulator (12 lanes / voxel), 1 = E and B
 // (6 lanes), 2 = rhof; one x plane covers all (iy, iz) incl. ghosts
