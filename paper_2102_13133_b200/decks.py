@@ -134,3 +134,47 @@ class Harris:
             sids.append(sid)
         ctx.upload_fields(self.fields(g))
         return sids
+
+
+@dataclasses.dataclass(frozen=True)
+class LPI:
+    """Laser-plasma interaction deck (BASELINE configs[3]): a laser launched
+    from a soft source near the low x wall into a plasma slab, absorbing
+    (Mur) field walls and absorbing particle walls on both x faces, periodic
+    in y and z.  Units: c = 1, omega_pe = 1 at unit weight (per-particle
+    q = -h^3/ppc, m = h^3/ppc), so n / n_cr = 1 / omega0^2.  Not expressible
+    in the reference, which is periodic only."""
+
+    n: tuple = (400, 2, 2)
+    h: float = 0.2
+    dt: float = 0.1
+    ppc: int = 8
+    omega0: float = 3.1622776601683795  # n / n_cr = 0.1
+    e0: float = 1e-3                     # laser field amplitude (a0 = e0 / omega0)
+    laser_ix: int = 20
+    ramp_steps: float = 40.0
+    slab: tuple = (150, 250)             # cells [ix_lo, ix_hi] holding plasma
+    mi_me: float = 100.0
+    u_th: float = 0.01
+
+    def grid(self):
+        from . import make_grid
+        return make_grid(self.n, self.h, dt=self.dt)
+
+    def species(self):
+        v = self.h ** 3 / self.ppc
+        return [("electron", -v, v, self.u_th), ("ion", v, self.mi_me * v, self.u_th / math.sqrt(self.mi_me))]
+
+    def load(self, ctx, seed: int = 5):
+        from . import FBC_MUR, PBC_ABSORB
+        g = ctx.grid
+        nslab = (self.slab[1] - self.slab[0] + 1) * g.ny * g.nz
+        sids = []
+        for name, q, m, uth in self.species():
+            sid = ctx.add_species(name, q, m, self.ppc * nslab + 65536)
+            ctx.load_slab(sid, self.ppc, uth, (0.0, 0.0, 0.0), seed, ix_lo=self.slab[0], ix_hi=self.slab[1])
+            sids.append(sid)
+        for side in (0, 1):
+            ctx.set_x_boundary(side, PBC_ABSORB, FBC_MUR)
+        ctx.set_laser(self.laser_ix, self.e0, self.omega0, pol=1, ramp_steps=self.ramp_steps)
+        return sids

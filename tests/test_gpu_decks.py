@@ -144,3 +144,29 @@ def test_harris_decomposed_tracks_oracle():
                 assert np.abs(gp[3:6] - wp[3:6]).max() <= 1e-4 * max(1.0, np.abs(wp[3:6]).max())
     for e in slabs.values():
         e.ctx.close()
+
+
+@pytest.mark.parametrize("omega0,transmits", [(3.1622776601683795, True), (0.5, False)])
+def test_lpi_underdense_transmits_overdense_reflects(omega0, transmits):
+    """LPI deck (BASELINE configs[3]): n / n_cr = 1 / omega0^2 = 0.1 lets the
+    laser through the slab with its vacuum amplitude; n / n_cr = 4 reflects
+    it (evanescent beyond a few skin depths).  The sin^2 switch-on lasts
+    three laser periods so its spectrum stays below omega_pe; e0 = 0.05 sits
+    far above the thermal-noise radiation of the 8-ppc slab (~4e-4 beyond it,
+    measured with the laser off: tools/lpi_probe.py)."""
+    import paper_2102_13133_b200 as pic
+    from paper_2102_13133_b200.decks import LPI
+    d = LPI(omega0=omega0, e0=0.05, ramp_steps=3 * 2 * np.pi / omega0 / 0.1)
+    g = d.grid()
+    with pic.Context(g) as ctx:
+        d.load(ctx)
+        for _ in range(1000):  # t = 100 c / omega_pe
+            ctx.step()
+        ey = ctx.download_fields()[F["ey"]].reshape(g.nz + 2, g.ny + 2, g.nx + 2)[1, 1, 1:-1]
+        lo, hi = ctx.absorbed_counts()
+    beyond = np.abs(ey[275:375]).max()
+    if transmits:
+        assert beyond > 0.7 * d.e0, beyond
+    else:
+        assert beyond < 0.1 * d.e0, beyond
+    assert lo + hi < 0.01 * d.ppc * 101 * g.ny * g.nz * 2  # the slab stays put
