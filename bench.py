@@ -78,6 +78,21 @@ def _harris_config():
 
 CONFIGS["harris"] = _harris_config()
 
+
+def _lpi_config():
+    """configs[3]: laser-plasma interaction (paper_2102_13133_b200/decks.py):
+    2048 x 64 x 64 cells (h = 0.2 c/omega_pe), an n/n_cr = 0.1 slab over x
+    cells 257..1792 with 64 ppc of electrons and ions (805 M particles), a
+    laser (a0 = 0.05) from a soft source near the low wall, Mur field walls
+    and absorbing particle walls in x; periodic in y, z."""
+    from paper_2102_13133_b200.decks import LPI
+    d = LPI(n=(2048, 64, 64), ppc=64, slab=(257, 1792), e0=0.05 * 3.1622776601683795, laser_ix=40)
+    return dict(n=2048, h=d.h, dt=d.dt, sort_interval=20, deck=d,
+                species=[(name, q, m, d.ppc, uth, (0.0, 0.0, 0.0)) for name, q, m, uth in d.species()])
+
+
+CONFIGS["lpi"] = _lpi_config()
+
 BYTES_PER_PUSH = 64  # 32 B record read + 32 B record written (SURVEY §8d)
 
 
@@ -282,7 +297,7 @@ def run_ours(args, rank, world):
 
     # --- e2e through the host-buffer C-ABI call --------------------------------
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and getattr(deck, "laser_ix", None) is None:  # walled decks: no pic_step_host
         e2e = run_e2e(pic, ctx, sids, npart, args, world)
     ctx.close()
     return dict(ms=ms, npart=npart, launches=launches, clocks=clk, phases=ph, push_rate_kernel=push_rate_kernel,
@@ -303,18 +318,33 @@ def run_ours_decomposed(args, rank, world):
     cfg = CONFIGS[args.config]
     n = cfg["n"]
     deck = cfg.get("deck")
+    lpi = deck is not None and hasattr(deck, "laser_ix")
+    walls = None
     if deck:  # weak scaling: the global box grows in x, (nx N) x ny x nz
         import dataclasses
-        deck = dataclasses.replace(deck, n=(deck.n[0] * world, deck.n[1], deck.n[2]))
-        geom = SlabGeometry(*deck.n, world, h=(cfg["h"],) * 3, dt=cfg["dt"])
+        NX0 = deck.n[0]
+        deck = dataclasses.replace(deck, n=(NX0 * world, deck.n[1], deck.n[2]))
+        if lpi:  # the slab keeps its distance from the far wall
+            deck = dataclasses.replace(deck, slab=(deck.slab[0], deck.n[0] - (NX0 - deck.slab[1])))
+            walls = (pic.PBC_ABSORB, pic.FBC_MUR)
+        geom = SlabGeometry(*deck.n, world, h=(cfg["h"],) * 3, dt=cfg["dt"], walls=walls)
     else:
         geom = SlabGeometry(n * world, n, n, world, h=(cfg["h"],) * 3, dt=cfg["dt"])
-    slab = CudaSlab(geom.local_grid(), rank, rank == 0, device=args.device)
+    slab = CudaSlab(geom.local_grid(), rank, rank == 0, device=args.device, walls=walls, world=world)
     sim = DecomposedSim(geom, {rank: slab}, DistTransport(rank, world))
     ctx = slab.ctx
     g = geom.local_grid()
     sids = []
-    if deck:
+    if lpi:
+        x0 = geom.x0(rank)
+        lo, hi = max(deck.slab[0], x0 + 1) - x0, min(deck.slab[1], x0 + g.nx) - x0
+        for name, q, m, uth in deck.species():
+            sid = sim.add_species(name, q, m, int(deck.ppc * g.interior * 1.02) + 65536)
+            if lo <= hi:
+                ctx.load_slab(sid, deck.ppc, uth, (0.0, 0.0, 0.0), seed=1234 + 7919 * rank, ix_lo=lo, ix_hi=hi)
+            sids.append(sid)
+        sim.set_laser(deck.laser_ix, deck.e0, deck.omega0, pol=1, ramp_steps=deck.ramp_steps)
+    elif deck:
         for name, q, m, uth, drift, sheet in deck.species():
             sid = sim.add_species(name, q, m, int(deck.ppc * g.interior * 1.02) + 65536)
             ctx.load_harris(sid, deck.ppc, uth, drift, seed=1234 + 7919 * rank, **sheet)
@@ -567,7 +597,8 @@ def main():
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic (device counter-RNG load: uniform offsets, drifting Maxwellian momenta"
-                + (", sech^2 Harris weights, A_y fields)" if cfg.get("deck") else ")"),
+                + {"harris": ", sech^2 Harris weights, A_y fields)",
+                   "lpi": " in the plasma slab; laser soft source, Mur / absorbing x walls)"}.get(args.config, ")"),
         "config": {"workload": args.config, "cells": f"{gl.nx}x{gl.ny}x{gl.nz}", "particles_per_gpu": res["npart"],
                    "ppc": sum(s[3] for s in cfg["species"]), "dt": g.dt, "sort_interval": cfg["sort_interval"],
                    "parallelism": f"x-slab decomposition over {world} GPUs (NCCL halo + migration)"

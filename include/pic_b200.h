@@ -196,8 +196,10 @@ int pic_set_x_open(pic_context* ctx, int x_open, int low_wraps);
  *   fields     PIC_FBC_PEC      conductor: tangential E = 0 on the wall;
  *              PIC_FBC_MUR      first-order Mur absorbing condition on the
  *                               tangential E at the wall (normal incidence).
- * Both sides must be periodic or both walls; not with decomposition
- * (pic_set_x_open).  Push variants 0 (deterministic), 42 and 43. */
+ * pic_step needs both sides periodic or both walls; on an x-decomposed
+ * slab (pic_set_x_open) a wall side is the global boundary and the host
+ * sequences the step (pic_wall_stage).  Push variants 42 and 43 and the
+ * deterministic path. */
 #define PIC_PBC_PERIODIC 0
 #define PIC_PBC_ABSORB 1
 #define PIC_PBC_REFLECT 2
@@ -208,6 +210,22 @@ int pic_set_x_boundary(pic_context* ctx, int side, int particle_bc, int field_bc
 /* particles absorbed through the low / high x wall since the last call
  * (synchronises) */
 int pic_absorbed_counts(pic_context* ctx, uint64_t out[2], int reset);
+/* The wall / laser / emitter pieces of the step for hosts that sequence it
+ * themselves (the decomposed driver: on an x-open slab a wall side is the
+ * global boundary, the other side keeps exchanging).  pic_step runs them at:
+ *   FOLD      after the pushes, before the y/z current folds (accumulator x
+ *             ghost planes of wall sides: mirror fold / drop)
+ *   AFTER_B   after each advance_b(frac) (B_x on the high wall plane)
+ *   BEFORE_E  before the E update (Mur's saved planes)
+ *   AFTER_E   after the E update (laser source, wall E; advances the
+ *             laser / emitter clock by one step)
+ *   EMIT      after the pushes (emitter hooks) */
+#define PIC_STAGE_FOLD 0
+#define PIC_STAGE_AFTER_B 1
+#define PIC_STAGE_BEFORE_E 2
+#define PIC_STAGE_AFTER_E 3
+#define PIC_STAGE_EMIT 4
+int pic_wall_stage(pic_context* ctx, int stage, float frac);
 
 /* Laser: a soft source on the node plane x = (ix - 1) hx — after every E
  * update E_pol += dt (2 e0 / hx) s(t) g(y, z) on that plane (a current sheet

@@ -102,6 +102,7 @@ class Laser(C.Structure):
 
 
 PBC_PERIODIC, PBC_ABSORB, PBC_REFLECT = 0, 1, 2
+STAGE_FOLD, STAGE_AFTER_B, STAGE_BEFORE_E, STAGE_AFTER_E, STAGE_EMIT = 0, 1, 2, 3, 4
 FBC_PERIODIC, FBC_PEC, FBC_MUR = 0, 1, 2
 
 
@@ -142,6 +143,7 @@ def lib() -> C.CDLL:
         "pic_species_load_harris": [P, C.c_int, C.c_int, C.c_float, F32, C.c_uint64, C.POINTER(Sheet)],
         "pic_species_load_slab": [P, C.c_int, C.c_int, C.c_float, F32, C.c_uint64, C.c_int, C.c_int],
         "pic_set_x_boundary": [P, C.c_int, C.c_int, C.c_int],
+        "pic_wall_stage": [P, C.c_int, C.c_float],
         "pic_absorbed_counts": [P, C.POINTER(C.c_uint64), C.c_int],
         "pic_set_laser": [P, C.POINTER(Laser)],
         "pic_set_emitter": [P, C.c_int, C.c_int, C.c_int, C.c_float, F32, C.c_uint64],
@@ -321,6 +323,10 @@ class Context:
     # --- non-periodic x boundaries, laser, emitter (pic_set_x_boundary ...) ---
     def set_x_boundary(self, side: int, particle_bc: int, field_bc: int):
         check(lib().pic_set_x_boundary(self._h, side, particle_bc, field_bc))
+
+    def wall_stage(self, stage: int, frac: float = 0.0):
+        """pic_wall_stage: STAGE_FOLD / AFTER_B / BEFORE_E / AFTER_E / EMIT."""
+        check(lib().pic_wall_stage(self._h, stage, frac))
 
     def absorbed_counts(self, reset: bool = False):
         out = (C.c_uint64 * 2)()

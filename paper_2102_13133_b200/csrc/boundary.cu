@@ -31,6 +31,7 @@ __global__ void wall_fold_kernel(GridC g, float* __restrict__ acc) {
   const long long P = (long long)g.pny * g.pnz;
   if (t >= 2 * P) return;
   const int side = (int)(t / P);
+  if (g.wall_p[side] == PIC_PBC_PERIODIC) return;  // an exchange side (decomposed)
   const long long r = t - side * P;
   const int iy = (int)(r % g.pny), iz = (int)(r / g.pny);
   const int gx = side ? g.nx + 1 : 0, bx = side ? g.nx : 1;
@@ -83,9 +84,10 @@ __global__ void wall_e_kernel(GridC g, float* __restrict__ f, const float* __res
   const long long P = (long long)g.pny * g.pnz;
   if (t >= 2 * P) return;
   const int side = (int)(t / P);
+  const int fb = g.wall_f[side];
+  if (fb == PIC_FBC_PERIODIC) return;  // an exchange side (decomposed)
   const long long r = t - side * P;
   const int iy = (int)(r % g.pny), iz = (int)(r / g.pny);
-  const int fb = g.wall_f[side];
   const size_t vw = (size_t)voxel_of(g, wall_plane_ix(g, side, 0), iy, iz);
   const size_t vi = (size_t)voxel_of(g, wall_plane_ix(g, side, 1), iy, iz);
   float* ey = f + (size_t)F_EY * g.V;
@@ -203,16 +205,17 @@ void set_x_boundary(Context& c, int side, int pbc, int fbc) {
   if (fbc < PIC_FBC_PERIODIC || fbc > PIC_FBC_MUR) throw UsageError("x boundary: unknown field bc");
   if ((pbc == PIC_PBC_PERIODIC) != (fbc == PIC_FBC_PERIODIC))
     throw UsageError("x boundary: particles and fields must both be periodic or both walls");
-  if (c.gc.xopen && !has_walls(c)) throw UsageError("x boundary: walls on an x-decomposed (x-open) context");
   c.gc.wall_p[side] = pbc;
   c.gc.wall_f[side] = fbc;
-  // one side may be set before the other; check_walls refuses a step with
-  // a single wall
+  // one side may be set before the other; check_walls refuses a pic_step
+  // with a single wall.  On a decomposed (x-open) slab a wall side is the
+  // global boundary, the other side keeps exchanging.
   const bool any = has_walls(c);
-  c.gc.xopen = any ? 1 : 0;
-  c.gc.x_low_wraps = 0;
-  if (any)
+  c.gc.xopen = (any || c.decomposed) ? 1 : 0;
+  if (any) {
+    if (c.gc.wall_p[0]) c.gc.x_low_wraps = 0;
     for (auto& s : c.species) ensure_mig_lists(c, s);
+  }
 }
 
 void check_walls(const Context& c, bool deterministic) {
@@ -221,6 +224,34 @@ void check_walls(const Context& c, bool deterministic) {
     throw UsageError("x boundary: both x sides must be walls (or both periodic)");
   if (!deterministic && c.push_variant != 42 && c.push_variant != 43)
     throw UsageError("x boundary: supported by push variants 42 / 43 and the deterministic path");
+}
+
+// The wall / laser / emitter pieces of the step, for hosts that sequence the
+// step themselves (the decomposed driver, domain.py); pic_step calls them in
+// the same places.
+void wall_stage(Context& c, int stage, float frac) {
+  const bool walls = has_walls(c);
+  switch (stage) {
+    case PIC_STAGE_FOLD:
+      if (walls) launch_wall_fold(c);
+      break;
+    case PIC_STAGE_AFTER_B:
+      if (walls) launch_wall_b(c, frac);
+      break;
+    case PIC_STAGE_BEFORE_E:
+      if (walls) launch_wall_e_save(c);
+      break;
+    case PIC_STAGE_AFTER_E:
+      launch_laser(c);
+      if (walls) launch_wall_e(c);
+      ++c.steps_done;
+      break;
+    case PIC_STAGE_EMIT:
+      if (!c.emitters.empty()) run_emitters(c);
+      break;
+    default:
+      throw UsageError("wall_stage: unknown stage");
+  }
 }
 
 // After a species' push: absorbed particles (recorded as x emigrants) are
@@ -257,6 +288,7 @@ void launch_wall_e(Context& c) {
 }
 
 void launch_wall_b(Context& c, float frac) {
+  if (c.gc.wall_f[1] == PIC_FBC_PERIODIC) return;  // B_x of the high wall plane only
   const float fdt = frac * c.grid.dt;
   wall_bx_kernel<<<nblk((long long)c.gc.ny * c.gc.nz), 256, 0, c.stream>>>(c.gc, c.f, -fdt / c.grid.hy,
                                                                            fdt / c.grid.hz);

@@ -223,25 +223,22 @@ static void step_prologue(Context& c) {
 // after each B half step, Mur's saved planes, the laser source and the wall
 // E condition around the E update.
 static void step_epilogue(Context& c) {
-  const bool walls = has_walls(c);
   c.phase_begin(Context::kPhScatter);
-  if (walls) launch_wall_fold(c);
+  wall_stage(c, PIC_STAGE_FOLD, 0.f);
   launch_ghost_fold(c);
   c.phase_end();
   c.phase_begin(Context::kPhField);
   launch_advance_b(c, 0.5f);
-  if (walls) launch_wall_b(c, 0.5f);
+  wall_stage(c, PIC_STAGE_AFTER_B, 0.5f);
   launch_ghost_sync(c);
-  if (walls) launch_wall_e_save(c);
+  wall_stage(c, PIC_STAGE_BEFORE_E, 0.f);
   launch_unload_advance_e(c, true, true);
-  launch_laser(c);
-  if (walls) launch_wall_e(c);
+  wall_stage(c, PIC_STAGE_AFTER_E, 0.f);
   launch_ghost_sync(c);
   launch_advance_b(c, 0.5f);
-  if (walls) launch_wall_b(c, 0.5f);
+  wall_stage(c, PIC_STAGE_AFTER_B, 0.5f);
   launch_ghost_sync(c);
   c.phase_end();
-  ++c.steps_done;
 }
 
 void step(Context& c, unsigned flags) {
@@ -258,7 +255,7 @@ void step(Context& c, unsigned flags) {
       launch_advance_p(c, s, exact);
     if (walls && (c.gc.wall_p[0] == PIC_PBC_ABSORB || c.gc.wall_p[1] == PIC_PBC_ABSORB)) absorb_compact(c, s);
   }
-  if (!c.emitters.empty()) run_emitters(c);
+  wall_stage(c, PIC_STAGE_EMIT, 0.f);
   c.phase_end();
   step_epilogue(c);
 }
@@ -722,6 +719,13 @@ int pic_step_host(pic_context* ctx, unsigned flags, float* const* lanes7, int32_
 
 int pic_set_x_boundary(pic_context* ctx, int side, int particle_bc, int field_bc) {
   return guard([&] { set_x_boundary(C_(ctx), side, particle_bc, field_bc); });
+}
+
+int pic_wall_stage(pic_context* ctx, int stage, float frac) {
+  return guard([&] {
+    wall_stage(C_(ctx), stage, frac);
+    check_launch();
+  });
 }
 
 int pic_absorbed_counts(pic_context* ctx, uint64_t out[2], int reset) {

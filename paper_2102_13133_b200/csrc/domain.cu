@@ -148,8 +148,9 @@ void ensure_mig_lists(Context& c, Species& s) {
 }
 
 void set_x_open(Context& c, bool open, bool low_wraps) {
-  if (has_walls(c)) throw UsageError("x-open: the context has x walls (pic_set_x_boundary)");
-  c.gc.xopen = open ? 1 : 0;
+  if (!open && has_walls(c)) throw UsageError("x-open: the context has x walls (pic_set_x_boundary)");
+  c.decomposed = open;
+  c.gc.xopen = (open || has_walls(c)) ? 1 : 0;
   c.gc.x_low_wraps = low_wraps ? 1 : 0;
   if (open)
     for (auto& s : c.species) ensure_mig_lists(c, s);

@@ -89,6 +89,7 @@ struct Context {
   };
   std::vector<Emitter> emitters;
   long long steps_done = 0;
+  bool decomposed = false;  // pic_set_x_open: x faces exchanged by the host
   cudaEvent_t events[64] = {};
 
   enum ScratchSlot {
@@ -165,6 +166,7 @@ void launch_wall_b(Context& c, float frac);
 void launch_laser(Context& c);
 void run_emitters(Context& c);
 void load_slab(Context& c, Species& s, int ppc, float u_th, const float drift[3], uint64_t seed, int lo, int hi);
+void wall_stage(Context& c, int stage, float frac);
 void set_x_open(Context& c, bool open, bool low_wraps);
 // halo planes: kind 0 = accumulator (12 lanes / voxel), 1 = E and B
 // (6 lanes), 2 = rhof; one x plane covers all (iy, iz) incl. ghosts

@@ -32,15 +32,17 @@ import dataclasses
 
 import numpy as np
 
-from . import (HALO_ACCUMULATOR, HALO_FIELDS, HALO_RHO, PIC_DETERMINISTIC, PIC_EXACT_GYRATION, F, Context,
-               UsageError, make_grid)
+from . import (HALO_ACCUMULATOR, HALO_FIELDS, HALO_RHO, PIC_DETERMINISTIC, PIC_EXACT_GYRATION, STAGE_AFTER_B,
+               STAGE_AFTER_E, STAGE_BEFORE_E, STAGE_EMIT, STAGE_FOLD, F, Context, UsageError, make_grid)
 
 DOWN, UP = 0, 1  # message travels to the low (DOWN) or high (UP) neighbour
 
 
 @dataclasses.dataclass(frozen=True)
 class SlabGeometry:
-    """Equal slabs of a global periodic box along x."""
+    """Equal slabs of a global box along x: periodic, or with walls = (particle
+    bc, field bc) on the two global x faces (pic_set_x_boundary; the outer
+    slabs own them, no exchange crosses them)."""
 
     NX: int
     NY: int
@@ -48,6 +50,11 @@ class SlabGeometry:
     world: int
     h: tuple = (1.0, 1.0, 1.0)
     dt: float | None = None
+    walls: tuple | None = None
+
+    def crosses_wall(self, rank: int, d: int) -> bool:
+        """A message from `rank` in direction d would cross a global wall."""
+        return self.walls is not None and ((rank == 0 and d == DOWN) or (rank == self.world - 1 and d == UP))
 
     def __post_init__(self):
         if self.world < 1 or self.NX % self.world:
@@ -192,12 +199,17 @@ def slab_stream(device: int = 0):
 class CudaSlab:
     """Engine adapter: one x-open sm_100a context (the product path)."""
 
-    def __init__(self, grid, rank: int, low_wraps: bool, device: int = 0):
+    def __init__(self, grid, rank: int, low_wraps: bool, device: int = 0, walls=None, world: int = 1):
         import torch
         self.torch = torch
         self.device = torch.device("cuda", device)
         self.ctx = Context(grid, device)
-        self.ctx.set_x_open(True, low_wraps)
+        self.ctx.set_x_open(True, low_wraps and walls is None)
+        if walls is not None:  # the outer slabs own the global walls
+            if rank == 0:
+                self.ctx.set_x_boundary(0, *walls)
+            if rank == world - 1:
+                self.ctx.set_x_boundary(1, *walls)
         self.stream = slab_stream(device)
         self.ctx.set_stream(self.stream.cuda_stream)
         self.grid = grid
@@ -258,6 +270,9 @@ class CudaSlab:
     def read_counts(self, t):
         return [int(x) for x in t.tolist()]
 
+    def wall_stage(self, stage, frac=0.0):
+        self.ctx.wall_stage(stage, frac)
+
     # diagnostics pieces
     def clear_rho(self):
         self.ctx.clear_rho()
@@ -293,6 +308,7 @@ class DecomposedSim:
         self.nspecies = 0
         self._bufs = {}
         self.on_mark = None  # optional callable(phase, begin) for timing
+        self.absorbed = [0, 0]  # particles this process's slabs lost through the low / high wall
 
     def add_species(self, name, q, m, capacity_per_slab):
         sids = {r: e.add_species(name, q, m, capacity_per_slab) for r, e in self.slabs.items()}
@@ -317,7 +333,7 @@ class DecomposedSim:
         for r, e in self.slabs.items():
             nb = e.halo_bytes(kind)
             for d in (DOWN, UP):
-                if send_ix[d] is None:
+                if send_ix[d] is None or g.crosses_wall(r, d):
                     continue
                 sb = self._buf(r, (tag, "s", d), nb)
                 e.halo_pack(kind, send_ix[d], sb, zero_after)
@@ -328,15 +344,16 @@ class DecomposedSim:
         for r, e in self.slabs.items():
             nb = e.halo_bytes(kind)
             for d in (DOWN, UP):
-                if send_ix[d] is None:
+                src = g.high(r) if d == DOWN else g.low(r)  # a DOWN message comes from the high side
+                if send_ix[d] is None or g.crosses_wall(src, d):
                     continue
                 rb = self._buf(r, (tag, "r", d), nb)
-                src = g.high(r) if d == DOWN else g.low(r)  # a DOWN message comes from the high side
                 full.append((src, r, d, rb))
         self._run(msgs, full)
         for r, e in self.slabs.items():
             for d in (DOWN, UP):
-                if send_ix[d] is None:
+                src = g.high(r) if d == DOWN else g.low(r)
+                if send_ix[d] is None or g.crosses_wall(src, d):
                     continue
                 e.halo_unpack(kind, recv_ix[d], self._buf(r, (tag, "r", d), e.halo_bytes(kind)), accumulate)
 
@@ -361,11 +378,15 @@ class DecomposedSim:
         for r, e in self.slabs.items():
             for d in (DOWN, UP):
                 dst = g.low(r) if d == DOWN else g.high(r)
-                sends.append((r, dst, d, e.count_buffer([counts[r][d]]), None))
+                if g.crosses_wall(r, d):  # particles leaving through an absorbing wall
+                    self.absorbed[d] += counts[r][d]
+                else:
+                    sends.append((r, dst, d, e.count_buffer([counts[r][d]]), None))
                 src = g.high(r) if d == DOWN else g.low(r)
-                recvs.append((src, r, d, e.count_buffer([0])))
+                if not g.crosses_wall(src, d):
+                    recvs.append((src, r, d, e.count_buffer([0])))
         self._run(sends, recvs)
-        incoming = {}
+        incoming = {(r, d): 0 for r in self.slabs for d in (DOWN, UP)}
         for src, r, d, buf in recvs:
             incoming[(r, d)] = self.slabs[r].read_counts(buf)[0]
         # 2) payloads (32 B records), packed while the stores compact
@@ -373,12 +394,15 @@ class DecomposedSim:
         for r, e in self.slabs.items():
             lo = self._buf(r, ("mig", "s", DOWN), 32 * counts[r][DOWN])
             hi = self._buf(r, ("mig", "s", UP), 32 * counts[r][UP])
-            e.migrate_pack(sid, lo, hi)
-            sends.append((r, g.low(r), DOWN, lo, None))
-            sends.append((r, g.high(r), UP, hi, None))
+            e.migrate_pack(sid, lo, hi)  # a wall side's buffer is packed and dropped
+            if not g.crosses_wall(r, DOWN):
+                sends.append((r, g.low(r), DOWN, lo, None))
+            if not g.crosses_wall(r, UP):
+                sends.append((r, g.high(r), UP, hi, None))
             for d in (DOWN, UP):
                 src = g.high(r) if d == DOWN else g.low(r)
-                recvs.append((src, r, d, self._buf(r, ("mig", "r", d), 32 * incoming[(r, d)])))
+                if not g.crosses_wall(src, d):
+                    recvs.append((src, r, d, self._buf(r, ("mig", "r", d), 32 * incoming[(r, d)])))
         self._run(sends, recvs)
         # 3) append: from the low neighbour (UP messages) first, then the high
         for r, e in self.slabs.items():
@@ -394,6 +418,7 @@ class DecomposedSim:
         nx = self.geom.nx
         self._plane_exchange(HALO_ACCUMULATOR, (0, nx + 1), (nx, 1), True, True, "accfold")
         for e in self.slabs.values():
+            self._wall(e, STAGE_FOLD)
             e.fold_yz()
         self._plane_exchange(HALO_ACCUMULATOR, (None, nx), (None, 0), False, False, "accghost")
 
@@ -404,6 +429,10 @@ class DecomposedSim:
         self._plane_exchange(HALO_FIELDS, (1, nx), (nx + 1, 0), False, False, "fields")
 
     # --- SimState::step ---------------------------------------------------------
+    def _wall(self, e, stage, frac=0.0):
+        if self.geom.walls is not None:
+            e.wall_stage(stage, frac)
+
     def step(self, deterministic=False, exact_gyration=False):
         flags = (PIC_DETERMINISTIC if deterministic else 0) | (PIC_EXACT_GYRATION if exact_gyration else 0)
         mark = self.on_mark or (lambda phase, begin: None)
@@ -415,16 +444,28 @@ class DecomposedSim:
             mark("push", False)
         for sid in range(self.nspecies):
             self.migrate(sid)
+        for e in self.slabs.values():
+            self._wall(e, STAGE_EMIT)
         self.fold_accumulator()
         for e in self.slabs.values():
             e.advance_b(0.5)
+            self._wall(e, STAGE_AFTER_B, 0.5)
         self.sync_fields()
         for e in self.slabs.values():
+            self._wall(e, STAGE_BEFORE_E)
             e.unload_advance_e()
+            self._wall(e, STAGE_AFTER_E)
         self.sync_fields()
         for e in self.slabs.values():
             e.advance_b(0.5)
+            self._wall(e, STAGE_AFTER_B, 0.5)
         self.sync_fields()
+
+    def set_laser(self, ix_global: int, e0: float, omega: float, **kw):
+        """The laser plane (global node index) on the slab that owns it."""
+        r, ix = divmod(ix_global - 1, self.geom.nx)
+        if r in self.slabs:
+            self.slabs[r].ctx.set_laser(ix + 1, e0, omega, **kw)
 
     # --- diagnostics (SimState::refresh_charge_diagnostics + current_diagnostics)
     def diagnostics(self):

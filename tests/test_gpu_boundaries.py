@@ -244,4 +244,79 @@ def test_walls_usage_errors():
         ctx.set_x_boundary(1, PBC_ABSORB, FBC_MUR)
         ctx.step()
         with pytest.raises(pic.UsageError):
-            ctx.set_x_open(True)
+            ctx.set_x_open(False)  # walls need the x faces open
+
+
+# --------------------------------------------------------------------- decomposed
+def _decomposed(world, NX, NY, NZ, walls, dt, h=1.0):
+    from paper_2102_13133_b200.domain import CudaSlab, DecomposedSim, LocalTransport, SlabGeometry
+    geom = SlabGeometry(NX, NY, NZ, world=world, h=(h,) * 3, dt=dt, walls=walls)
+    slabs = {r: CudaSlab(geom.local_grid(), r, r == 0, walls=walls, world=world) for r in range(world)}
+    return geom, slabs, DecomposedSim(geom, slabs, LocalTransport())
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_decomposed_laser_between_mur_walls_matches_single_domain(world):
+    """No particles: the decomposed field solve with the global Mur walls and
+    the laser on one slab equals the single-domain run bit for bit."""
+    import paper_2102_13133_b200 as pic
+    NX, NY, NZ, dt = 96, 3, 2, 0.5
+    g = pic.make_grid((NX, NY, NZ), 1.0, dt=dt)
+    with pic.Context(g) as ctx:
+        ctx.set_x_boundary(0, PBC_ABSORB, FBC_MUR)
+        ctx.set_x_boundary(1, PBC_ABSORB, FBC_MUR)
+        ctx.set_laser(30, 1e-2, 0.6, pol=2, ramp_steps=10, waist=1.5, y0=1.5, z0=1.0)
+        for _ in range(150):
+            ctx.step()
+        want = ctx.download_fields()
+    geom, slabs, sim = _decomposed(world, NX, NY, NZ, (PBC_ABSORB, FBC_MUR), dt)
+    sim.set_laser(30, 1e-2, 0.6, pol=2, ramp_steps=10, waist=1.5, y0=1.5, z0=1.0)
+    for _ in range(150):
+        sim.step()
+    got = geom.join_fields([slabs[r].ctx.download_fields() for r in range(world)])
+    for e in slabs.values():
+        e.ctx.close()
+    for name in ("ex", "ey", "ez", "cbx", "cby", "cbz"):
+        a = got[F[name]].reshape(NZ + 2, NY + 2, NX + 2)[1:-1, 1:-1, 1:-1]
+        b = want[F[name]].reshape(NZ + 2, NY + 2, NX + 2)[1:-1, 1:-1, 1:-1]
+        assert (a.view(np.uint32) == b.view(np.uint32)).all(), name
+    assert np.abs(want[F["ez"]]).max() > 1e-3
+
+
+@pytest.mark.parametrize("pbc", [PBC_REFLECT, PBC_ABSORB])
+def test_decomposed_walls_particles(pbc):
+    """Ballistic particles across 3 slabs with global walls: reflection is the
+    exact mirror of the periodic run, absorption removes exactly the leavers."""
+    g_nx, ny, nz = 9, 3, 4
+    import paper_2102_13133_b200 as pic
+    g = pic.make_grid((g_nx, ny, nz), 1.0, dt=0.25)
+    p, ids = _ballistic_state(g, 3000, seed=5)
+    steps = 16
+    want_p, want_ids, wraps = _periodic_reference(g, p, ids, steps)
+    geom, slabs, sim = _decomposed(3, g_nx, ny, nz, (pbc, FBC_PEC if pbc == PBC_REFLECT else FBC_MUR), 0.25)
+    sid = sim.add_species("e", Q, M, ids.size)
+    for r, part in enumerate(geom.split(p, ids)):
+        slabs[r].ctx.upload_species(sid, *part)
+    for _ in range(steps):
+        sim.step()
+    parts = [slabs[r].ctx.download_species(sid) for r in range(3)]
+    gp = np.concatenate([q for q, _ in parts], axis=1)
+    gids = np.concatenate([geom.to_global_ids(r, parts[r][1]) for r in range(3)])
+    for e in slabs.values():
+        e.ctx.close()
+    gp, gids = _by_tag(gp, gids)
+    if pbc == PBC_ABSORB:
+        keep = wraps == 0
+        assert sim.absorbed == [int((wraps == -1).sum()), int((wraps == 1).sum())]
+        assert (gids == want_ids[keep]).all()
+        assert (gp.view(np.uint32) == want_p[:, keep].view(np.uint32)).all()
+    else:
+        pitch = g.nx + 2
+        ix_w = want_ids % pitch
+        exp_ids = np.where(wraps != 0, want_ids - ix_w + (g.nx + 1 - ix_w), want_ids).astype(np.int32)
+        exp_p = want_p.copy()
+        m = wraps != 0
+        exp_p[0, m] = -want_p[0, m]
+        exp_p[3, m] = -want_p[3, m]
+        assert (gids == exp_ids).all()
+        assert (gp.view(np.uint32) == exp_p.view(np.uint32)).all()
