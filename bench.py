@@ -503,7 +503,21 @@ def run_e2e(pic, ctx, sids, npart, args, world):
             "d2h_bytes_per_step": b_out, "steps": k, "ms_per_step": dt / k * 1e3}
 
 
+_OUT_FD = None
+
+
+def emit(obj):
+    """The one JSON line on the real stdout: everything else the run prints
+    (NCCL's version banner, library chatter) goes to stderr (main() points
+    fd 1 at fd 2)."""
+    os.write(_OUT_FD if _OUT_FD is not None else 1, (json.dumps(obj) + "\n").encode())
+
+
 def main():
+    global _OUT_FD
+    _OUT_FD = os.dup(1)
+    sys.stdout.flush()
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -528,13 +542,13 @@ def main():
         if rank != 0:
             return
         if cfg.get("deck"):
-            print(json.dumps({"impl": "reference", "unavailable": f"the reference's deck text cannot express the "
-                              f"{args.config} deck (built through the API here)"}))
+            emit({"impl": "reference", "unavailable": f"the reference's deck text cannot express the "
+                              f"{args.config} deck (built through the API here)"})
             return
         r = cpu_reference(args.config, max(1, min(args.steps, 3)), max(1, min(args.warmup, 1)),
                           sample_n=args.cpu_sample_n)
         if r is None:
-            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libminipic_ref.so not built"}))
+            emit({"impl": "reference", "unavailable": "oracle/_ref/libminipic_ref.so not built"})
             return
         line = {
             "impl": "reference", "metric": "particle pushes/sec/GPU (advance_p, whole step)", "value": r["value"],
@@ -546,7 +560,7 @@ def main():
             "e2e": {"value": r["value"], "unit": "particle pushes/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
         }
-        print(json.dumps(line))
+        emit(line)
         return
 
     if world > 1 or args.decomposed:
@@ -620,7 +634,7 @@ def main():
         "gpu_launches": res["launches"],
         "clocks": res["clocks"],
     }
-    print(json.dumps(line))
+    emit(line)
     if world > 1 or args.decomposed:
         import torch.distributed as dist
         dist.destroy_process_group()
