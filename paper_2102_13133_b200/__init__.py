@@ -511,6 +511,12 @@ class Context:
         fn.argtypes = [C.c_void_p, C.c_int]
         check(fn(self._h, variant))
 
+    def _set_graphs(self, on: bool):
+        """Benchmarking hook (not in the public C header): pic_step as CUDA graphs."""
+        fn = lib().pic_internal_set_graphs
+        fn.argtypes = [C.c_void_p, C.c_int]
+        check(fn(self._h, int(on)))
+
     def _set_sort_variant(self, variant: int):
         """Benchmarking hook (not in the public C header): sort strategy."""
         fn = lib().pic_internal_set_sort_variant

@@ -178,6 +178,8 @@ Context* make_context(int device, const pic_grid& g) {
 void destroy_context(Context* c) {
   if (!c) return;
   cudaSetDevice(c->device);
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+  c->graphs.clear();
   c->release();
   delete c;
 }
@@ -675,13 +677,91 @@ int pic_sort_particles(pic_context* ctx, int species, int order) {
     check_launch();
   });
 }
+// SimState::step as one CUDA graph launch.  The fast step
+// has no host synchronisation, so it is captured once per configuration —
+// flags, push variant and every species' (pos, mom, n); the sort swaps the
+// record buffers, so two graphs alternate — and relaunched.  Steps with host
+// work between kernels run as plain launches: deterministic replay (segment
+// count read back), absorbing walls (compaction counts), emitters (n grows),
+// the laser (host-computed amplitude), phase timing (host events).
+static bool graph_ok(const Context& c, unsigned flags) {
+  if (flags & PIC_DETERMINISTIC) return false;
+  if (c.phase_timing || !c.emitters.empty() || c.laser.e0 != 0.f) return false;
+  if (c.gc.wall_p[0] == PIC_PBC_ABSORB || c.gc.wall_p[1] == PIC_PBC_ABSORB) return false;
+  return c.use_graphs;
+}
+
+static std::vector<uint64_t> graph_key(const Context& c, unsigned flags) {
+  std::vector<uint64_t> k{flags, (uint64_t)c.push_variant, (uint64_t)c.gc.wall_p[0], (uint64_t)c.gc.wall_p[1],
+                          (uint64_t)c.gc.wall_f[0], (uint64_t)c.gc.wall_f[1], (uint64_t)(uintptr_t)c.stream};
+  for (const auto& s : c.species) {
+    k.push_back((uint64_t)(uintptr_t)s.pos);
+    k.push_back((uint64_t)(uintptr_t)s.mom);
+    k.push_back((uint64_t)s.n);
+  }
+  return k;
+}
+
+void step_graphed(Context& c, unsigned flags) {
+  if (!graph_ok(c, flags)) {
+    step(c, flags);
+    return;
+  }
+  const auto key = graph_key(c, flags);
+  for (auto& g : c.graphs) {
+    if (g.key == key) {
+      CUDA_OK(cudaGraphLaunch(g.exec, c.stream));
+      c.count_launch(g.launches);
+      ++c.steps_done;
+      return;
+    }
+  }
+  if (c.graph_seen != key) {  // first step of a configuration: plain (allocates scratch, sets attributes)
+    c.graph_seen = key;
+    step(c, flags);
+    return;
+  }
+  const uint64_t l0 = c.launches;
+  const long long sd = c.steps_done;
+  cudaGraph_t graph = nullptr;
+  CUDA_OK(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    step(c, flags);
+  } catch (...) {
+    cudaStreamEndCapture(c.stream, &graph);
+    if (graph) cudaGraphDestroy(graph);
+    throw;
+  }
+  CUDA_OK(cudaStreamEndCapture(c.stream, &graph));
+  Context::Graph g;
+  g.key = key;
+  g.launches = c.launches - l0;
+  CUDA_OK(cudaGraphInstantiate(&g.exec, graph, 0));
+  CUDA_OK(cudaGraphDestroy(graph));
+  c.launches = l0;
+  c.steps_done = sd;
+  if (c.graphs.size() >= 4) {
+    CUDA_OK(cudaGraphExecDestroy(c.graphs.front().exec));
+    c.graphs.erase(c.graphs.begin());
+  }
+  c.graphs.push_back(g);
+  CUDA_OK(cudaGraphLaunch(g.exec, c.stream));
+  c.count_launch(g.launches);
+  ++c.steps_done;
+}
+
 int pic_step(pic_context* ctx, unsigned flags) {
   return guard([&] {
     if (C_(ctx).gc.xopen && !has_walls(C_(ctx)))
       throw UsageError("pic_step: x-open (decomposed) context; the host sequences the step");
-    step(C_(ctx), flags);
+    step_graphed(C_(ctx), flags);
     check_launch();
   });
+}
+
+// Not in the public header: CUDA graphs for pic_step on / off (benchmarking).
+int pic_internal_set_graphs(pic_context* ctx, int on) {
+  return guard([&] { C_(ctx).use_graphs = on != 0; });
 }
 
 int pic_step_host(pic_context* ctx, unsigned flags, float* const* lanes7, int32_t* const* ids) {

@@ -90,6 +90,15 @@ struct Context {
   std::vector<Emitter> emitters;
   long long steps_done = 0;
   bool decomposed = false;  // pic_set_x_open: x faces exchanged by the host
+  // pic_step as CUDA graphs (capi.cu step_graphed): a few configurations
+  struct Graph {
+    std::vector<uint64_t> key;
+    cudaGraphExec_t exec = nullptr;
+    uint64_t launches = 0;
+  };
+  std::vector<Graph> graphs;
+  std::vector<uint64_t> graph_seen;
+  bool use_graphs = true;
   cudaEvent_t events[64] = {};
 
   enum ScratchSlot {

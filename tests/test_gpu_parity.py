@@ -144,7 +144,7 @@ def test_advance_p_parity(pic, orc, dims, n, u, deterministic):
     assert (wids != _push_case.ids0).mean() > 0.02
 
 
-PUSH_VARIANTS = list(range(47))
+PUSH_VARIANTS = list(range(48))
 
 
 @pytest.mark.parametrize("variant", PUSH_VARIANTS)
@@ -380,3 +380,37 @@ def test_empty_species_and_zero_particles(pic):
         assert ctx.species_count(sid) == 0
         f = ctx.download_fields()
         assert not f.any()
+
+
+def test_graph_step_matches_plain_launches(pic, orc):
+    """pic_step replays a captured CUDA graph from the third step of a
+    configuration on (and a second graph after the sort swaps the record
+    buffers): particle state and fields match plain launches within the fast
+    mode's atomic-order tolerance; the launch counter keeps counting."""
+    g = pic.make_grid((16, 12, 10), 1.0, dt=0.25)
+    species = [(-1.0 / 8, 1.0 / 8, 8, 0.1, (0.05, 0.0, 0.0)), (1.0 / 8, 100.0 / 8, 4, 0.01, (0.0, 0.0, 0.0))]
+    outs = []
+    for graphs in (False, True):
+        with pic.Context(g) as ctx:
+            ctx._set_graphs(graphs)
+            sids = []
+            for si, (q, m, ppc, uth, drift) in enumerate(species):
+                sid = ctx.add_species(f"s{si}", q, m, ppc * g.interior)
+                ctx.load_synthetic(sid, ppc, uth, drift, seed=3)
+                sids.append(sid)
+            l0 = ctx.launch_count()
+            for k in range(12):
+                ctx.step()
+                if k == 5:
+                    for s in sids:
+                        ctx.sort_particles(s)
+            ctx.synchronize()
+            launches = ctx.launch_count() - l0
+            outs.append(([ctx.download_species(s) for s in sids], ctx.download_fields(), launches))
+    (pa, fa, la), (pb, fb, lb) = outs
+    for (p1, i1), (p2, i2) in zip(pa, pb):
+        assert (i1 == i2).mean() > 0.999
+        same = i1 == i2
+        assert np.abs(p1[:, same] - p2[:, same]).max() <= 1e-4 * max(1.0, np.abs(p1).max())
+    assert np.abs(fa - fb).max() <= 1e-3 * max(np.abs(fa).max(), 1e-12)
+    assert la == lb
