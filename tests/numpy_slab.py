@@ -27,7 +27,7 @@ from oracle.bindings import Orc
 
 
 class NumpySlab:
-    def __init__(self, grid, rank: int, low_wraps: bool):
+    def __init__(self, grid, rank: int, low_wraps: bool, walls=None, world: int = 1):
         self.g = OGrid(grid.nx, grid.ny, grid.nz, grid.hx, grid.hy, grid.hz, grid.dt)
         self.grid = grid
         self.rank = rank
@@ -38,6 +38,10 @@ class NumpySlab:
         self.interp = np.zeros((18, self.V), np.float32)
         self.sp = []  # [q, m, p7, ids, mig_low, mig_high]
         self.pnx, self.pny, self.pnz = grid.nx + 2, grid.ny + 2, grid.nz + 2
+        # global x walls (absorbing particles, PEC fields only) on the outer slabs
+        if walls is not None:
+            assert tuple(walls) == (1, 1), "numpy engine: absorbing particle walls with PEC fields only"
+        self.wall = [walls is not None and rank == 0, walls is not None and rank == world - 1]
 
     # --- geometry helpers ---------------------------------------------------------
     def _ix(self, ids):
@@ -91,7 +95,36 @@ class NumpySlab:
         self.orc.advance_b(self.g, self.f, frac)
 
     def sync_yz(self):
+        # the oracle sync is fully periodic; an open x face keeps its x ghost
+        # planes (neighbour halo or wall), whose own y / z ghosts are then
+        # synced like the CUDA kernel's y / z faces over the padded x range
+        keep = {ix: self.f[:, self._plane(ix)].copy() for ix in (0, self.grid.nx + 1)}
         self.orc.ghost_sync(self.g, self.f)
+        ny, nz = self.grid.ny, self.grid.nz
+        for ix, vals in keep.items():
+            self.f[:, self._plane(ix)] = vals
+            f = self.f.reshape(16, self.pnz, self.pny, self.pnx)
+            f[:, :, 0, ix] = f[:, :, ny, ix]
+            f[:, :, ny + 1, ix] = f[:, :, 1, ix]
+            f[:, 0, :, ix] = f[:, nz, :, ix]
+            f[:, nz + 1, :, ix] = f[:, 1, :, ix]
+
+    def wall_stage(self, stage, frac=0.0):
+        """pic_wall_stage for absorbing particle / PEC field walls: FOLD drops
+        the accumulator's ghost plane beyond a wall, AFTER_E zeroes the
+        tangential E on the wall plane (and E_x outside)."""
+        nx = self.grid.nx
+        for side in (0, 1):
+            if not self.wall[side]:
+                continue
+            ghost = 0 if side == 0 else nx + 1
+            if stage == 0:  # STAGE_FOLD
+                self.acc[self._plane(ghost)] = 0
+            elif stage == 3:  # STAGE_AFTER_E
+                wall_plane = self._plane(1 if side == 0 else nx + 1)
+                self.f[1, wall_plane] = 0
+                self.f[2, wall_plane] = 0
+                self.f[0, self._plane(ghost)] = 0
 
     def unload_advance_e(self):
         a = self.acc.copy()

@@ -245,3 +245,75 @@ def test_cuda_slab_deterministic_mode_runs():
     sim.synchronize()
     n = sum(e.ctx.species_count(s) for e in slabs.values() for s in range(len(SPECIES)))
     assert n == sum(ids.size for _, _, _, ids in state)
+
+
+# --------------------------------------------------------------- global x walls
+def _run_numpy_walls(geom, ranks, transport, state, steps):
+    from tests.numpy_slab import NumpySlab
+    slabs = {r: NumpySlab(geom.local_grid(), r, r == 0, walls=geom.walls, world=geom.world) for r in ranks}
+    sim = DecomposedSim(geom, slabs, transport)
+    for si, (q, m, p, ids) in enumerate(state):
+        sid = sim.add_species(f"s{si}", q, m, 1 << 20)
+        parts = geom.split(p, ids)
+        for r in ranks:
+            slabs[r].upload(sid, *parts[r])
+    for _ in range(steps):
+        sim.step()
+    parts = {r: [(s[2].copy(), s[3].copy()) for s in slabs[r].sp] for r in ranks}
+    return sim, parts, {r: slabs[r].f.copy() for r in ranks}
+
+
+def _gloo_walls_worker(rank, world, port, tmp):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.bindings import Orc
+        geom = SlabGeometry(*DIMS, world=world, dt=0.25, walls=(1, 1))
+        state = _global_state(Orc(), _og(geom.global_grid()))
+        sim, parts, fields = _run_numpy_walls(geom, [rank], DistTransport(rank, world), state, STEPS)
+        np.savez(os.path.join(tmp, f"r{rank}.npz"),
+                 **{f"p{si}": parts[rank][si][0] for si in range(len(SPECIES))},
+                 **{f"i{si}": parts[rank][si][1] for si in range(len(SPECIES))},
+                 f=fields[rank], absorbed=np.array(sim.absorbed))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_global_walls():
+    """Absorbing / conducting global x walls (pic_set_x_boundary on the outer
+    slabs): two processes over gloo against one slab holding the whole box —
+    nothing crosses a wall, the leavers are dropped on the owning rank, and
+    fields and particles agree."""
+    import socket
+
+    import torch.multiprocessing as mp
+    from oracle.bindings import Orc
+    world = 2
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    with tempfile.TemporaryDirectory() as tmp:
+        mp.spawn(_gloo_walls_worker, args=(world, port, tmp), nprocs=world, join=True)
+        res = [np.load(os.path.join(tmp, f"r{r}.npz")) for r in range(world)]
+    geom2 = SlabGeometry(*DIMS, world=world, dt=0.25, walls=(1, 1))
+    geom1 = SlabGeometry(*DIMS, world=1, dt=0.25, walls=(1, 1))
+    state = _global_state(Orc(), _og(geom1.global_grid()))
+    sim1, parts1, fields1 = _run_numpy_walls(geom1, [0], LocalTransport(), state, STEPS)
+    absorbed2 = res[0]["absorbed"] + res[1]["absorbed"]
+    assert list(absorbed2) == sim1.absorbed and sum(sim1.absorbed) > 0
+    for si in range(len(SPECIES)):
+        gp = np.concatenate([res[r][f"p{si}"] for r in range(world)], axis=1)
+        gi = np.concatenate([geom2.to_global_ids(r, res[r][f"i{si}"]) for r in range(world)])
+        gp, gi = _by_tag(gp, gi)
+        wp, wi = _by_tag(parts1[0][si][0], geom1.to_global_ids(0, parts1[0][si][1]))
+        assert gp.shape == wp.shape
+        assert (gi == wi).mean() > 0.999
+        assert np.abs(gp[3:6] - wp[3:6]).max() <= 1e-4 * max(1.0, np.abs(wp[3:6]).max())
+    gf = geom2.join_fields([res[r]["f"] for r in range(world)])
+    wf = geom1.join_fields([fields1[0]])
+    for lane in (0, 1, 2, 4, 5, 6):
+        a = gf[lane].reshape(DIMS[2] + 2, DIMS[1] + 2, DIMS[0] + 2)[1:-1, 1:-1, 1:-1]
+        b = wf[lane].reshape(DIMS[2] + 2, DIMS[1] + 2, DIMS[0] + 2)[1:-1, 1:-1, 1:-1]
+        assert np.abs(a - b).max() <= 1e-4 * max(np.abs(b).max(), 1e-12), lane
