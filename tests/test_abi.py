@@ -40,17 +40,19 @@ def test_library_is_sm100a_only():
 
 
 def test_kernels_are_the_cuda_path():
-    """The push kernel is real sm_100a SASS using vector reductions into the
-    accumulator and no local-memory spills on the hot path."""
+    """The default push (advance_p_lean, variant 43) is real sm_100a SASS:
+    TMA bulk copies of the particle slices, vector reductions into the
+    accumulator, no local-memory traffic; the sort ranks with MATCH."""
     sass = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
     funcs = re.split(r"\n\s+Function : ", sass)
-    push = [f for f in funcs if f.startswith("_ZN4picb14advance_p_fastILi1ELb0E")]
+    push = [f for f in funcs if f.startswith("_ZN4picb14advance_p_leanILi8ELi6ELb0ELb0ELb0ELi4ELi0E")]
     assert push, "default advance_p kernel not found"
     body = push[0]
     assert "REDG.E.ADD.F32x4" in body
-    assert "MATCH" in body  # warp voxel grouping
-    tma = [f for f in funcs if "advance_p_tma" in f.split("\n", 1)[0]]
-    assert tma and "UBLKCP" in tma[0]  # TMA bulk copies in the staged variant
+    assert "UBLKCP" in body  # cp.async.bulk (TMA) slice loads / stores
+    assert "LDL" not in body and "STL" not in body  # no spills
+    scatter = [f for f in funcs if "radix_scatter_kernel" in f.split("\n", 1)[0]]
+    assert scatter and any("MATCH" in f for f in scatter)
 
 
 def test_product_never_imports_the_oracle():
