@@ -78,6 +78,7 @@ void Context::release() {
     cudaFree(s.mom);
     cudaFree(s.pos_alt);
     cudaFree(s.mom_alt);
+    cudaFree(s.perm);
     cudaFree(s.mig_idx);
     cudaFree(s.mig_count);
   }
@@ -156,6 +157,7 @@ Context* make_context(int device, const pic_grid& g) {
     CUDA_OK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     if (const char* v = std::getenv("PIC_PUSH_VARIANT")) c->push_variant = std::atoi(v);  // profiling knob
     if (const char* v = std::getenv("PIC_SORT_VARIANT")) set_sort_variant(*c, std::atoi(v));  // profiling knob
+    if (const char* v = std::getenv("PIC_SORT_DEFER")) c->sort_defer = std::atoi(v) != 0;     // profiling knob
     const size_t V = (size_t)gc.V;
     CUDA_OK(cudaMalloc(&c->f, F_COUNT * V * sizeof(float)));
     CUDA_OK(cudaMalloc(&c->interp, kInterpF4 * V * sizeof(float4)));
@@ -200,9 +202,17 @@ void quiesce(Context& c) {
   }
 }
 
-Species& species_at(Context& c, int sid) {
+// A species for an entry point: any deferred sort permutation is applied
+// first (the reference's order is what every caller observes); the push and
+// the count take it as it is (species_ref).
+static Species& species_ref(Context& c, int sid) {
   if (sid < 0 || sid >= (int)c.species.size()) throw UsageError("species index out of range");
   return c.species[(size_t)sid];
+}
+Species& species_at(Context& c, int sid) {
+  Species& s = species_ref(c, sid);
+  materialize(c, s);
+  return s;
 }
 
 // SimState::step (proj/src/sim.cpp:143-183).  unload_currents is fused into
@@ -271,6 +281,7 @@ void step(Context& c, unsigned flags) {
 // pinned (pic_host_register) for the copies to overlap.
 static void step_host(Context& c, unsigned flags, float* const* lanes7, int32_t* const* ids) {
   const bool exact = (flags & PIC_EXACT_GYRATION) != 0;
+  for (auto& s : c.species) s.perm_pending = false;  // the host arrays replace the device records
   size_t nmax = 0;
   for (auto& s : c.species) nmax = std::max(nmax, s.n);
   const size_t chunk = std::max<size_t>(1, std::min<size_t>(nmax, c.host_chunk));
@@ -442,7 +453,7 @@ int pic_species_create(pic_context* ctx, const char* name, float q, float m, siz
 }
 
 int pic_species_count(pic_context* ctx, int species, size_t* out_n) {
-  return guard([&] { *out_n = species_at(C_(ctx), species).n; });
+  return guard([&] { *out_n = species_ref(C_(ctx), species).n; });
 }
 
 static void validate_ids(const pic_grid& g, const int32_t* ids, size_t n) {
@@ -623,7 +634,7 @@ int pic_load_interpolators(pic_context* ctx) {
 int pic_advance_p(pic_context* ctx, int species, unsigned flags) {
   return guard([&] {
     Context& c = C_(ctx);
-    Species& s = species_at(c, species);
+    Species& s = species_ref(c, species);  // the push applies a deferred sort itself
     if (flags & PIC_DETERMINISTIC)
       launch_advance_p_deterministic(c, s, (flags & PIC_EXACT_GYRATION) != 0);
     else
@@ -698,6 +709,7 @@ static std::vector<uint64_t> graph_key(const Context& c, unsigned flags) {
     k.push_back((uint64_t)(uintptr_t)s.pos);
     k.push_back((uint64_t)(uintptr_t)s.mom);
     k.push_back((uint64_t)s.n);
+    k.push_back(s.perm_pending ? 1u : 0u);
   }
   return k;
 }
@@ -927,6 +939,7 @@ int pic_compute_div_errors(pic_context* ctx) {
 int pic_refresh_charge_diagnostics(pic_context* ctx) {
   return guard([&] {
     Context& c = C_(ctx);
+    materialize_all(c);
     launch_clear_rho(c);
     for (auto& s : c.species) launch_deposit_rho(c, s);
     launch_compute_div_errors(c);
@@ -960,6 +973,7 @@ int pic_diagnostics(pic_context* ctx, pic_diag* out, float* kinetic, size_t kine
   return guard([&] {
     Context& c = C_(ctx);
     if (!out) throw UsageError("diagnostics: null output");
+    materialize_all(c);
     if (kinetic_cap < c.species.size() || (!kinetic && !c.species.empty()))
       throw UsageError("diagnostics: kinetic[] smaller than the species count");
     quiesce(c);

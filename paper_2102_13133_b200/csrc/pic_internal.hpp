@@ -53,6 +53,12 @@ struct Species {
   unsigned* mig_count = nullptr;
   unsigned* mig_idx = nullptr;
   unsigned mig_cap = 0;
+  // Deferred sort permutation (sort.cu): after a blocked sort the records
+  // stay where they are and perm[j] names the record that belongs at j; the
+  // next default push gathers through it and writes the sorted store, any
+  // other consumer materialises it first (materialize()).
+  unsigned* perm = nullptr;  // cap entries (lazy)
+  bool perm_pending = false;
 };
 
 struct Context {
@@ -77,6 +83,7 @@ struct Context {
   int sort_variant = 0;
   int sort_radix_bits = 9;  // LSD digit width (passes = ceil(key bits / width), widths evened out)
   int sort_match = 1;       // group equal digits with match.any (0: per-bit ballots)
+  bool sort_defer = true;   // blocked sorts leave the permutation to the next push
   int num_sms = 148;
   // non-periodic x boundaries (boundary.cu): absorbed particle counts per
   // side, the laser source, emitter hooks, steps taken (laser clock)
@@ -206,6 +213,9 @@ void exclusive_scan_u32(Context& c, const unsigned* in, unsigned* out, size_t n)
 void radix_sort_pairs(Context& c, const unsigned* keys, const unsigned* vals, size_t n,
                       int key_bits, unsigned** keys_out, unsigned** vals_out);
 void sort_species(Context& c, Species& s, int order);
+// apply a deferred sort permutation (no-op when none is pending)
+void materialize(Context& c, Species& s);
+void materialize_all(Context& c);
 // Sort strategies (benchmarking): 0 = LSD radix, 9-bit digits, equal digits
 // grouped with match.any (default); 1 = tiled counting sort; 2 = radix,
 // 8-bit digits; 3 = radix, 9-bit, per-bit ballot grouping; 4 = 8-bit, ballot.

@@ -600,7 +600,8 @@ static void radix_pass_bits(Context& c, int bits, const unsigned* kin, const uns
 // index.  first_hist: the first pass's per-tile histogram is already in the
 // table.  keys_out == nullptr: the sorted keys are not wanted.
 static void radix_sort_impl(Context& c, const unsigned* keys, const unsigned* vals, size_t n, int key_bits,
-                            bool first_hist, unsigned** keys_out, unsigned** vals_out) {
+                            bool first_hist, unsigned** keys_out, unsigned** vals_out,
+                            unsigned* last_vals = nullptr) {
   unsigned* ka = static_cast<unsigned*>(c.scratch_bytes(Context::kScrKeyA, n * 4));
   unsigned* va = static_cast<unsigned*>(c.scratch_bytes(Context::kScrValA, n * 4));
   unsigned* kb = static_cast<unsigned*>(c.scratch_bytes(Context::kScrKeyB, n * 4));
@@ -616,6 +617,7 @@ static void radix_sort_impl(Context& c, const unsigned* keys, const unsigned* va
   for (int p = 0, shift = 0; p < passes; ++p, shift += step) {
     const int bits = std::min(step, key_bits - shift);
     const bool last = p + 1 == passes;
+    if (last && last_vals) vout = last_vals;  // the permutation straight into its own buffer
     radix_pass_bits(c, bits, kin, vin, n, shift, ntiles, table, p == 0 && first_hist,
                     (last && !keys_out) ? nullptr : kout, vout);
     kin = kout;
@@ -632,8 +634,23 @@ void radix_sort_pairs(Context& c, const unsigned* keys, const unsigned* vals, si
   radix_sort_impl(c, keys, vals, n, key_bits, false, keys_out, vals_out);
 }
 
+void materialize(Context& c, Species& s) {
+  if (!s.perm_pending) return;
+  s.perm_pending = false;
+  if (s.n == 0) return;
+  permute_kernel<<<blocks_for(s.n), 256, 0, c.stream>>>(s.perm, s.n, s.pos, s.mom, s.pos_alt, s.mom_alt);
+  c.count_launch();
+  std::swap(s.pos, s.pos_alt);
+  std::swap(s.mom, s.mom_alt);
+}
+
+void materialize_all(Context& c) {
+  for (auto& s : c.species) materialize(c, s);
+}
+
 // sort_particles (particles.cpp:412-458).
 void sort_species(Context& c, Species& s, int order) {
+  materialize(c, s);
   const size_t n = s.n;
   if (n == 0) return;
   if (!s.pos_alt) {
@@ -672,6 +689,14 @@ void sort_species(Context& c, Species& s, int order) {
   }
   c.count_launch();
   unsigned* perm = nullptr;
+  if (order != PIC_SORT_INTERLEAVED && c.sort_defer) {
+    // blocked order, deferred: the next push gathers through the permutation
+    // (a separate gather pass reads and writes every record once more)
+    if (!s.perm) CUDA_OK(cudaMalloc(&s.perm, s.cap * sizeof(unsigned)));
+    radix_sort_impl(c, keys, nullptr, n, kbits, true, nullptr, nullptr, s.perm);
+    s.perm_pending = true;
+    return;
+  }
   if (order != PIC_SORT_INTERLEAVED) {
     radix_sort_impl(c, keys, nullptr, n, kbits, true, nullptr, &perm);
   } else {

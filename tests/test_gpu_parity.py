@@ -414,3 +414,32 @@ def test_graph_step_matches_plain_launches(pic, orc):
         assert np.abs(p1[:, same] - p2[:, same]).max() <= 1e-4 * max(1.0, np.abs(p1).max())
     assert np.abs(fa - fb).max() <= 1e-3 * max(np.abs(fa).max(), 1e-12)
     assert la == lb
+
+
+def test_deferred_sort_permutation(pic, orc):
+    """A blocked sort leaves its permutation to the next default push, which
+    gathers through it: the state after sort + push equals sort (applied) +
+    push, and a download between them sees the sorted order."""
+    g = pic.make_grid((14, 9, 7), 1.0, dt=0.25)
+    rng = np.random.default_rng(5)
+    p, ids = rand_particles(g, rng, 20000, sort=False)
+    p[3:6] *= 0.3
+    res = []
+    for mode in ("materialized", "deferred", "peek"):
+        with pic.Context(g) as ctx:
+            sid = ctx.add_species("s", -1.0 / 16, 1.0 / 16, ids.size)
+            ctx.upload_species(sid, p, ids)
+            ctx.sort_particles(sid)
+            if mode == "materialized":
+                ctx.download_species(sid)  # any entry point applies the permutation
+            if mode == "peek":
+                sp, sids = ctx.download_species(sid)
+                q, qi = p.copy(), ids.copy()
+                orc.sort(q, qi)
+                assert_bitwise(sids, qi, "sorted ids")
+                assert_bitwise(sp, q, "sorted lanes")
+            ctx.advance_p(sid)
+            res.append(ctx.download_species(sid))
+    for (a, ai), (b, bi) in zip(res[:-1], res[1:]):
+        assert_bitwise(ai, bi, "ids after push")
+        assert_bitwise(a, b, "lanes after push")
