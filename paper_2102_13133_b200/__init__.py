@@ -18,7 +18,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpic_b200.so")
+LIB_PATH = os.environ.get("PIC_LIB_PATH") or os.path.join(HERE, "libpic_b200.so")  # override: A/B builds
 
 PIC_EXACT_GYRATION = 0x1
 PIC_DETERMINISTIC = 0x2
