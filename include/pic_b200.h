@@ -198,8 +198,8 @@ int pic_set_x_open(pic_context* ctx, int x_open, int low_wraps);
  *                               tangential E at the wall (normal incidence).
  * pic_step needs both sides periodic or both walls; on an x-decomposed
  * slab (pic_set_x_open) a wall side is the global boundary and the host
- * sequences the step (pic_wall_stage).  Push variants 42 and 43 and the
- * deterministic path. */
+ * sequences the step (pic_wall_stage).  The default push (and variants
+ * 42-52) and the deterministic path. */
 #define PIC_PBC_PERIODIC 0
 #define PIC_PBC_ABSORB 1
 #define PIC_PBC_REFLECT 2

@@ -222,8 +222,8 @@ void check_walls(const Context& c, bool deterministic) {
   if (!has_walls(c)) return;
   if (!c.gc.wall_p[0] || !c.gc.wall_p[1])
     throw UsageError("x boundary: both x sides must be walls (or both periodic)");
-  if (!deterministic && c.push_variant != 42 && c.push_variant != 43)
-    throw UsageError("x boundary: supported by push variants 42 / 43 and the deterministic path");
+  if (!deterministic && (c.push_variant < 42 || c.push_variant > 52))
+    throw UsageError("x boundary: supported by push variants 42-52 and the deterministic path");
 }
 
 // The wall / laser / emitter pieces of the step, for hosts that sequence the

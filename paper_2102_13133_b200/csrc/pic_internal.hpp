@@ -78,7 +78,7 @@ struct Context {
   // first-segment moments (default); 20 = the same with per-particle weights;
   // 7 = TMA-staged CTA rounds with warp reduction;
   // 0 = one particle per thread; 1, 5, 6, 8, 9 = TMA-staged ablations; 2-4 = other ablations
-  int push_variant = 43;
+  int push_variant = 52;
   // sort_particles (blocked): 0 = LSD radix over (voxel, index), 1 = tiled counting sort (ablation)
   int sort_variant = 0;
   int sort_radix_bits = 9;  // LSD digit width (passes = ceil(key bits / width), widths evened out)

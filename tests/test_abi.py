@@ -40,12 +40,12 @@ def test_library_is_sm100a_only():
 
 
 def test_kernels_are_the_cuda_path():
-    """The default push (advance_p_lean, variant 43) is real sm_100a SASS:
+    """The default push (advance_p_lean, variant 52) is real sm_100a SASS:
     TMA bulk copies of the particle slices, vector reductions into the
     accumulator, no local-memory traffic; the sort ranks with MATCH."""
     sass = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
     funcs = re.split(r"\n\s+Function : ", sass)
-    push = [f for f in funcs if f.startswith("_ZN4picb14advance_p_leanILi8ELi6ELb0ELb0ELb0ELi4ELi0E")]
+    push = [f for f in funcs if f.startswith("_ZN4picb14advance_p_leanILi8ELi6ELb0ELb0ELb0ELi4ELi0ELb0ELb1E")]
     assert push, "default advance_p kernel not found"
     body = push[0]
     assert "REDG.E.ADD.F32x4" in body
