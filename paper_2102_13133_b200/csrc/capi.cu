@@ -96,7 +96,7 @@ void Context::release() {
     if (e) cudaEventDestroy(e);
   for (auto& e : ev_pool) cudaEventDestroy(e);
   ev_pool.clear();
-  for (int b = 0; b < 2; ++b) {
+  for (int b = 0; b < kMaxStage; ++b) {
     if (ev_in[b]) cudaEventDestroy(ev_in[b]);
     if (ev_packed[b]) cudaEventDestroy(ev_packed[b]);
     if (ev_unpacked[b]) cudaEventDestroy(ev_unpacked[b]);
@@ -158,6 +158,7 @@ Context* make_context(int device, const pic_grid& g) {
     if (const char* v = std::getenv("PIC_PUSH_VARIANT")) c->push_variant = std::atoi(v);  // profiling knob
     if (const char* v = std::getenv("PIC_SORT_VARIANT")) set_sort_variant(*c, std::atoi(v));  // profiling knob
     if (const char* v = std::getenv("PIC_SORT_DEFER")) c->sort_defer = std::atoi(v) != 0;     // profiling knob
+    if (const char* v = std::getenv("PIC_HOST_BUFS")) c->host_bufs = std::atoi(v);            // profiling knob
     const size_t V = (size_t)gc.V;
     CUDA_OK(cudaMalloc(&c->f, F_COUNT * V * sizeof(float)));
     CUDA_OK(cudaMalloc(&c->interp, kInterpF4 * V * sizeof(float4)));
@@ -288,20 +289,24 @@ static void step_host(Context& c, unsigned flags, float* const* lanes7, int32_t*
   if (!c.cs_in) {
     CUDA_OK(cudaStreamCreateWithFlags(&c.cs_in, cudaStreamNonBlocking));
     CUDA_OK(cudaStreamCreateWithFlags(&c.cs_out, cudaStreamNonBlocking));
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < Context::kMaxStage; ++b) {
       CUDA_OK(cudaEventCreateWithFlags(&c.ev_in[b], cudaEventDisableTiming));
       CUDA_OK(cudaEventCreateWithFlags(&c.ev_packed[b], cudaEventDisableTiming));
       CUDA_OK(cudaEventCreateWithFlags(&c.ev_unpacked[b], cudaEventDisableTiming));
       CUDA_OK(cudaEventCreateWithFlags(&c.ev_out[b], cudaEventDisableTiming));
     }
   }
-  if (c.hstage_bytes < chunk * 32) {
+  const int nb = std::min(std::max(c.host_bufs, 2), (int)Context::kMaxStage);
+  if (c.hstage_bytes < chunk * 32 || !c.hstage[nb - 1]) {
     CUDA_OK(cudaStreamSynchronize(c.stream));
     for (auto& p : c.hstage) {
       cudaFree(p);
       p = nullptr;
     }
-    for (auto& p : c.hstage) CUDA_OK(cudaMalloc(&p, chunk * 32));
+    for (int b = 0; b < nb; ++b) {
+      CUDA_OK(cudaMalloc(&c.hstage[b], chunk * 32));
+      CUDA_OK(cudaMalloc(&c.hstage[Context::kMaxStage + b], chunk * 32));
+    }
     c.hstage_bytes = chunk * 32;
   }
   step_prologue(c);
@@ -312,9 +317,9 @@ static void step_host(Context& c, unsigned flags, float* const* lanes7, int32_t*
     const size_t n = sp.n;
     for (size_t start = 0; start < n; start += chunk, ++it) {
       const size_t cnt = std::min(chunk, n - start);
-      const int b = (int)(it & 1);
+      const int b = (int)(it % (size_t)nb);
       char* in = static_cast<char*>(c.hstage[b]);
-      char* out = static_cast<char*>(c.hstage[2 + b]);
+      char* out = static_cast<char*>(c.hstage[Context::kMaxStage + b]);
       // H2D: 7 lane rows (host pitch n) + ids into in[b] once its last pack is done
       CUDA_OK(cudaStreamWaitEvent(c.cs_in, c.ev_packed[b], 0));
       CUDA_OK(cudaMemcpy2DAsync(in, cnt * 4, lanes7[si] + start, n * 4, cnt * 4, 7, cudaMemcpyHostToDevice,

@@ -133,8 +133,11 @@ struct Context {
   // host-buffer step pipeline (pic_step_host): copy-in / copy-out streams,
   // double-buffered staging, ordering events
   cudaStream_t cs_in = nullptr, cs_out = nullptr;
-  cudaEvent_t ev_in[2] = {}, ev_packed[2] = {}, ev_unpacked[2] = {}, ev_out[2] = {};
-  void* hstage[4] = {};  // in[0], in[1], out[0], out[1]
+  static constexpr int kMaxStage = 4;
+  int host_bufs = 2;  // staging buffers per direction (PIC_HOST_BUFS: 2-4; 3, 4 measured no faster)
+  cudaEvent_t ev_in[kMaxStage] = {}, ev_packed[kMaxStage] = {}, ev_unpacked[kMaxStage] = {},
+              ev_out[kMaxStage] = {};
+  void* hstage[2 * kMaxStage] = {};  // in[0..kMaxStage), out[0..kMaxStage)
   size_t hstage_bytes = 0;
   size_t host_chunk = (size_t)1 << 24;  // particles per pipelined chunk (16 M: measured best on B200/PCIe5)
 
