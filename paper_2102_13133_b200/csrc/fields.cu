@@ -54,10 +54,18 @@ unsigned interior_blocks(const GridC& g, int threads) {
 }
 
 // ---- load_interpolators (particles.cpp:48-110) ----------------------------
+// Each thread builds one voxel's record; the CTA's 256 records are staged in
+// shared memory and leave as contiguous 128-bit stores (a record per thread
+// stored directly is five 16-B stores 80 B apart per warp instruction: the
+// LSU throttled at half the DRAM bandwidth).
 __global__ void __launch_bounds__(256)
 load_interpolators_kernel(GridC g, Lanes L, float4* __restrict__ out) {
+  __shared__ float4 buf[256 * kInterpF4];
+  __shared__ long long sv[256];
   int ix, iy, iz;
-  if (!interior_coords(g, (long long)blockIdx.x * blockDim.x + threadIdx.x, ix, iy, iz)) return;
+  const bool valid = interior_coords(g, (long long)blockIdx.x * blockDim.x + threadIdx.x, ix, iy, iz);
+  sv[threadIdx.x] = valid ? (long long)voxel_of(g, ix, iy, iz) : -1;
+  if (valid) {
   const size_t v = (size_t)voxel_of(g, ix, iy, iz);
   const size_t sx = 1, sy = (size_t)g.sy, sz = (size_t)g.sz;
   const float* __restrict__ fex = L.p[F_EX];
@@ -91,28 +99,57 @@ load_interpolators_kernel(GridC g, Lanes L, float4* __restrict__ out) {
   r4.y = 0.5f * (w1 - w0);
   r4.z = 0.f;
   r4.w = 0.f;
-  float4* o = out + v * kInterpF4;
+  float4* o = buf + threadIdx.x * kInterpF4;
   o[0] = r0; o[1] = r1; o[2] = r2; o[3] = r3; o[4] = r4;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256 * kInterpF4; i += 256) {
+    const long long vv = sv[i / kInterpF4];
+    if (vv >= 0) out[vv * kInterpF4 + i % kInterpF4] = buf[i];
+  }
 }
 
 // ---- advance_b (fields.cpp:113-151) -----------------------------------------
 struct BCoef {
   float c1x, c2x, c1y, c2y, c1z, c2z;
 };
+// kVox voxels per thread, 256 apart (each round coalesced), every load of
+// every round issued before the first store: the one-voxel-per-thread form
+// stalled on load latency at half the DRAM bandwidth.
+constexpr int kBVox = 4;
 __global__ void __launch_bounds__(256)
 advance_b_kernel(GridC g, Lanes L, BCoef k) {
-  int ix, iy, iz;
-  if (!interior_coords(g, (long long)blockIdx.x * blockDim.x + threadIdx.x, ix, iy, iz)) return;
-  const size_t v = (size_t)voxel_of(g, ix, iy, iz);
   const size_t sx = 1, sy = (size_t)g.sy, sz = (size_t)g.sz;
   const float* __restrict__ ex = L.p[F_EX];
   const float* __restrict__ ey = L.p[F_EY];
   const float* __restrict__ ez = L.p[F_EZ];
-  const float exv = ex[v], eyv = ey[v], ezv = ez[v];
-  // dst = (dst + c1 * (p1 - p0)) + c2 * (q1 - q0)
-  L.p[F_BX][v] = (L.p[F_BX][v] + k.c1x * (ez[v + sy] - ezv)) + k.c2x * (ey[v + sz] - eyv);
-  L.p[F_BY][v] = (L.p[F_BY][v] + k.c1y * (ex[v + sz] - exv)) + k.c2y * (ez[v + sx] - ezv);
-  L.p[F_BZ][v] = (L.p[F_BZ][v] + k.c1z * (ey[v + sx] - eyv)) + k.c2z * (ex[v + sy] - exv);
+  float* __restrict__ bx = L.p[F_BX];
+  float* __restrict__ by = L.p[F_BY];
+  float* __restrict__ bz = L.p[F_BZ];
+  const long long base = (long long)blockIdx.x * (256 * kBVox) + threadIdx.x;
+  size_t v[kBVox];
+  bool ok[kBVox];
+  float e0[kBVox][3], e1[kBVox][6], b0[kBVox][3];
+#pragma unroll
+  for (int r = 0; r < kBVox; ++r) {
+    int ix, iy, iz;
+    ok[r] = interior_coords(g, base + r * 256, ix, iy, iz);
+    v[r] = ok[r] ? (size_t)voxel_of(g, ix, iy, iz) : (size_t)g.sz + (size_t)g.sy + 1;  // a valid interior address
+    const size_t w = v[r];
+    e0[r][0] = ex[w]; e0[r][1] = ey[w]; e0[r][2] = ez[w];
+    e1[r][0] = ez[w + sy]; e1[r][1] = ey[w + sz]; e1[r][2] = ex[w + sz];
+    e1[r][3] = ez[w + sx]; e1[r][4] = ey[w + sx]; e1[r][5] = ex[w + sy];
+    b0[r][0] = bx[w]; b0[r][1] = by[w]; b0[r][2] = bz[w];
+  }
+#pragma unroll
+  for (int r = 0; r < kBVox; ++r) {
+    if (!ok[r]) continue;
+    const size_t w = v[r];
+    // dst = (dst + c1 * (p1 - p0)) + c2 * (q1 - q0)
+    bx[w] = (b0[r][0] + k.c1x * (e1[r][0] - e0[r][2])) + k.c2x * (e1[r][1] - e0[r][1]);
+    by[w] = (b0[r][1] + k.c1y * (e1[r][2] - e0[r][0])) + k.c2y * (e1[r][3] - e0[r][2]);
+    bz[w] = (b0[r][2] + k.c1z * (e1[r][4] - e0[r][1])) + k.c2z * (e1[r][5] - e0[r][0]);
+  }
 }
 
 // ---- unload_currents (gather form) + advance_e --------------------------------
@@ -370,7 +407,7 @@ void launch_advance_b(Context& c, float frac) {
   k.c1x = -fdt * rhy; k.c2x = fdt * rhz;
   k.c1y = -fdt * rhz; k.c2y = fdt * rhx;
   k.c1z = -fdt * rhx; k.c2z = fdt * rhy;
-  advance_b_kernel<<<interior_blocks(c.gc, 256), 256, 0, c.stream>>>(c.gc, lanes_of(c), k);
+  advance_b_kernel<<<interior_blocks(c.gc, 256 * kBVox), 256, 0, c.stream>>>(c.gc, lanes_of(c), k);
   c.count_launch();
 }
 
