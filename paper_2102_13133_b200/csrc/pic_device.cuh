@@ -69,6 +69,14 @@ __device__ __forceinline__ int voxel_of(const GridC& g, int ix, int iy, int iz) 
 
 // Streaming 128-bit loads/stores for the particle records (each record is
 // touched exactly once per kernel).
+// Read-only gather that bypasses L1 (keeps L1 for the interpolator records).
+__device__ __forceinline__ float4 ld_na(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
 __device__ __forceinline__ float4 ld_stream(const float4* p) {
   float4 r;
   asm volatile("ld.global.cs.v4.f32 {%0,%1,%2,%3}, [%4];"
