@@ -144,7 +144,7 @@ def test_advance_p_parity(pic, orc, dims, n, u, deterministic):
     assert (wids != _push_case.ids0).mean() > 0.02
 
 
-PUSH_VARIANTS = list(range(53))
+PUSH_VARIANTS = list(range(55))
 
 
 @pytest.mark.parametrize("variant", PUSH_VARIANTS)
