@@ -139,15 +139,27 @@ radix_hist_kernel(const unsigned* __restrict__ keys, const float4* __restrict__ 
   unsigned key[kPer];
   const bool full = i0 + kPer <= n;
   if (FROM_POS) {
+    // records read coalesced (a thread's 16 consecutive records would be 16
+    // loads 256 B apart per warp instruction), keys written coalesced, then
+    // transposed through shared memory into the per-thread runs
+    __shared__ uint4 skeys[kTile / 4];
+    unsigned* sk = reinterpret_cast<unsigned*>(skeys);
 #pragma unroll
-    for (int k = 0; k < kPer; ++k) key[k] = (full || i0 + k < n) ? (unsigned)__float_as_int(ld_stream(pos + i0 + k).w) : 0u;
-    if (full) {
-      uint4* o = reinterpret_cast<uint4*>(keys_out + i0);
+    for (int k = 0; k < kPer; ++k) {
+      const int j = k * kThreads + threadIdx.x;
+      const size_t i = tbase + j;
+      const unsigned kv = i < n ? (unsigned)__float_as_int(ld_stream(pos + i).w) : 0u;
+      sk[j] = kv;
+      if (i < n) keys_out[i] = kv;
+    }
+    __syncthreads();
 #pragma unroll
-      for (int k = 0; k < kPer / 4; ++k) o[k] = make_uint4(key[4 * k], key[4 * k + 1], key[4 * k + 2], key[4 * k + 3]);
-    } else {
-      for (int k = 0; k < kPer; ++k)
-        if (i0 + k < n) keys_out[i0 + k] = key[k];
+    for (int k = 0; k < kPer / 4; ++k) {
+      const uint4 v = skeys[threadIdx.x * (kPer / 4) + k];
+      key[4 * k] = v.x;
+      key[4 * k + 1] = v.y;
+      key[4 * k + 2] = v.z;
+      key[4 * k + 3] = v.w;
     }
   } else if (full) {
     const uint4* in = reinterpret_cast<const uint4*>(keys + i0);
