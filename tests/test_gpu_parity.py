@@ -144,7 +144,7 @@ def test_advance_p_parity(pic, orc, dims, n, u, deterministic):
     assert (wids != _push_case.ids0).mean() > 0.02
 
 
-PUSH_VARIANTS = list(range(55))
+PUSH_VARIANTS = list(range(56))
 
 
 @pytest.mark.parametrize("variant", PUSH_VARIANTS)
