@@ -207,6 +207,12 @@ int pic_set_x_open(pic_context* ctx, int x_open, int low_wraps);
 #define PIC_FBC_PEC 1
 #define PIC_FBC_MUR 2
 int pic_set_x_boundary(pic_context* ctx, int side, int particle_bc, int field_bc);
+/* Any face: 0 = x low, 1 = x high, 2 = y low, 3 = y high, 4 = z low,
+ * 5 = z high (same conditions; the wall plane of a y / z face is the y / z
+ * node plane, tangential E = (E_z, E_x) / (E_x, E_y)).  y / z walls are
+ * single-domain only (not on an x-decomposed slab); pic_absorbed_counts
+ * then counts the low / high faces of every axis together. */
+int pic_set_boundary(pic_context* ctx, int face, int particle_bc, int field_bc);
 /* particles absorbed through the low / high x wall since the last call
  * (synchronises) */
 int pic_absorbed_counts(pic_context* ctx, uint64_t out[2], int reset);

@@ -143,6 +143,7 @@ def lib() -> C.CDLL:
         "pic_species_load_harris": [P, C.c_int, C.c_int, C.c_float, F32, C.c_uint64, C.POINTER(Sheet)],
         "pic_species_load_slab": [P, C.c_int, C.c_int, C.c_float, F32, C.c_uint64, C.c_int, C.c_int],
         "pic_set_x_boundary": [P, C.c_int, C.c_int, C.c_int],
+        "pic_set_boundary": [P, C.c_int, C.c_int, C.c_int],
         "pic_wall_stage": [P, C.c_int, C.c_float],
         "pic_absorbed_counts": [P, C.POINTER(C.c_uint64), C.c_int],
         "pic_set_laser": [P, C.POINTER(Laser)],
@@ -323,6 +324,10 @@ class Context:
     # --- non-periodic x boundaries, laser, emitter (pic_set_x_boundary ...) ---
     def set_x_boundary(self, side: int, particle_bc: int, field_bc: int):
         check(lib().pic_set_x_boundary(self._h, side, particle_bc, field_bc))
+
+    def set_boundary(self, face: int, particle_bc: int, field_bc: int):
+        """face 0-5: x low, x high, y low, y high, z low, z high (pic_set_boundary)."""
+        check(lib().pic_set_boundary(self._h, face, particle_bc, field_bc))
 
     def wall_stage(self, stage: int, frac: float = 0.0):
         """pic_wall_stage: STAGE_FOLD / AFTER_B / BEFORE_E / AFTER_E / EMIT."""

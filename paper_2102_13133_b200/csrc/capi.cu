@@ -266,7 +266,7 @@ void step(Context& c, unsigned flags) {
       launch_advance_p_deterministic(c, s, exact);
     else
       launch_advance_p(c, s, exact);
-    if (walls && (c.gc.wall_p[0] == PIC_PBC_ABSORB || c.gc.wall_p[1] == PIC_PBC_ABSORB)) absorb_compact(c, s);
+    if (walls && absorbing_walls(c)) absorb_compact(c, s);
   }
   wall_stage(c, PIC_STAGE_EMIT, 0.f);
   c.phase_end();
@@ -703,13 +703,13 @@ int pic_sort_particles(pic_context* ctx, int species, int order) {
 static bool graph_ok(const Context& c, unsigned flags) {
   if (flags & PIC_DETERMINISTIC) return false;
   if (c.phase_timing || !c.emitters.empty() || c.laser.e0 != 0.f) return false;
-  if (c.gc.wall_p[0] == PIC_PBC_ABSORB || c.gc.wall_p[1] == PIC_PBC_ABSORB) return false;
+  if (absorbing_walls(c)) return false;
   return c.use_graphs;
 }
 
 static std::vector<uint64_t> graph_key(const Context& c, unsigned flags) {
-  std::vector<uint64_t> k{flags, (uint64_t)c.push_variant, (uint64_t)c.gc.wall_p[0], (uint64_t)c.gc.wall_p[1],
-                          (uint64_t)c.gc.wall_f[0], (uint64_t)c.gc.wall_f[1], (uint64_t)(uintptr_t)c.stream};
+  std::vector<uint64_t> k{flags, (uint64_t)c.push_variant, (uint64_t)(uintptr_t)c.stream};
+  for (int f = 0; f < 6; ++f) k.push_back(((uint64_t)c.gc.wall_p[f] << 8) | (uint64_t)c.gc.wall_f[f]);
   for (const auto& s : c.species) {
     k.push_back((uint64_t)(uintptr_t)s.pos);
     k.push_back((uint64_t)(uintptr_t)s.mom);
@@ -816,6 +816,10 @@ int pic_step_host(pic_context* ctx, unsigned flags, float* const* lanes7, int32_
 
 int pic_set_x_boundary(pic_context* ctx, int side, int particle_bc, int field_bc) {
   return guard([&] { set_x_boundary(C_(ctx), side, particle_bc, field_bc); });
+}
+
+int pic_set_boundary(pic_context* ctx, int face, int particle_bc, int field_bc) {
+  return guard([&] { set_boundary(C_(ctx), face, particle_bc, field_bc); });
 }
 
 int pic_wall_stage(pic_context* ctx, int stage, float frac) {

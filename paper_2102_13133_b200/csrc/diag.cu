@@ -181,8 +181,8 @@ deposit_rho_kernel(GridC g, const float4* __restrict__ pos, const float4* __rest
   if (key < 0) return;
   const float* s = w;
   const int xh = (ix + 1 > g.nx && !g.xopen) ? 1 : ix + 1;  // x-decomposed: ghost, halo-added
-  const int yh = iy + 1 > g.ny ? 1 : iy + 1;
-  const int zh = iz + 1 > g.nz ? 1 : iz + 1;
+  const int yh = (iy + 1 > g.ny && !g.ywall) ? 1 : iy + 1;  // walled: the wall node plane
+  const int zh = (iz + 1 > g.nz && !g.zwall) ? 1 : iz + 1;
   atomicAdd(rho + voxel_of(g, ix, iy, iz), s[0]);
   atomicAdd(rho + voxel_of(g, xh, iy, iz), s[1]);
   atomicAdd(rho + voxel_of(g, ix, yh, iz), s[2]);

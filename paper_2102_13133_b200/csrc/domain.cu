@@ -148,7 +148,8 @@ void ensure_mig_lists(Context& c, Species& s) {
 }
 
 void set_x_open(Context& c, bool open, bool low_wraps) {
-  if (!open && has_walls(c)) throw UsageError("x-open: the context has x walls (pic_set_x_boundary)");
+  if (!open && (c.gc.wall_p[0] || c.gc.wall_p[1])) throw UsageError("x-open: the context has x walls (pic_set_x_boundary)");
+  if (open && (c.gc.ywall || c.gc.zwall)) throw UsageError("x-open: y / z walls are single-domain only");
   c.decomposed = open;
   c.gc.xopen = (open || has_walls(c)) ? 1 : 0;
   c.gc.x_low_wraps = low_wraps ? 1 : 0;
@@ -207,7 +208,7 @@ void halo_unpack(Context& c, int kind, int ix, const void* src, bool accumulate)
 
 void migrate_counts(Context& c, Species& s, size_t out[2]) {
   out[0] = out[1] = 0;
-  if (!c.gc.xopen || !s.mig_count) return;
+  if ((!c.gc.xopen && !c.gc.ywall && !c.gc.zwall) || !s.mig_count) return;
   unsigned h[2];
   CUDA_OK(cudaMemcpyAsync(h, s.mig_count, sizeof h, cudaMemcpyDeviceToHost, c.stream));
   CUDA_OK(cudaStreamSynchronize(c.stream));

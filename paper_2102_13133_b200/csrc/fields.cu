@@ -188,10 +188,12 @@ unload_advance_e_kernel(GridC g, Lanes L, const float* __restrict__ acc, ECoef k
     // x-decomposed: the x-1 neighbour of ix = 1 is the ghost plane filled
     // from the low neighbour; it precedes in the reference's sum order
     // unless this slab's low face is the global periodic boundary
+    // walled y / z: the -1 neighbour of the first cell is the ghost row,
+    // emptied by the wall fold
     const int xm = (ix == 1 && !g.xopen) ? g.nx : ix - 1;
-    const int ym = iy == 1 ? g.ny : iy - 1;
-    const int zm = iz == 1 ? g.nz : iz - 1;
-    const bool xmf = ix != 1 || (g.xopen && !g.x_low_wraps), ymf = iy != 1, zmf = iz != 1;
+    const int ym = (iy == 1 && !g.ywall) ? g.ny : iy - 1;
+    const int zm = (iz == 1 && !g.zwall) ? g.nz : iz - 1;
+    const bool xmf = ix != 1 || (g.xopen && !g.x_low_wraps), ymf = iy != 1 || g.ywall, zmf = iz != 1 || g.zwall;
     const float* a_000 = acc + (size_t)v * 12;
     const float* a_0y0 = acc + (size_t)voxel_of(g, ix, ym, iz) * 12;
     const float* a_00z = acc + (size_t)voxel_of(g, ix, iy, zm) * 12;
@@ -233,7 +235,8 @@ __global__ void __launch_bounds__(256)
 ghost_sync_kernel(GridC g, Lanes L) {
   long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   // x-decomposed: the x faces come from the neighbours (halo exchange)
-  const long long fx = g.xopen ? 0 : 2LL * g.pny * g.pnz, fy = 2LL * g.pnx * g.pnz, fz = 2LL * g.pnx * g.pny;
+  const long long fx = g.xopen ? 0 : 2LL * g.pny * g.pnz, fy = g.ywall ? 0 : 2LL * g.pnx * g.pnz,
+                  fz = g.zwall ? 0 : 2LL * g.pnx * g.pny;  // walled faces: wall conditions (boundary.cu)
   int ix, iy, iz;
   if (t < fx) {
     const int side = (int)(t & 1);
@@ -257,7 +260,8 @@ ghost_sync_kernel(GridC g, Lanes L) {
     return;
   }
   const size_t to = (size_t)voxel_of(g, ix, iy, iz);
-  const size_t from = (size_t)voxel_of(g, g.xopen ? ix : wrapc(ix, g.nx), wrapc(iy, g.ny), wrapc(iz, g.nz));
+  const size_t from = (size_t)voxel_of(g, g.xopen ? ix : wrapc(ix, g.nx), g.ywall ? iy : wrapc(iy, g.ny),
+                                      g.zwall ? iz : wrapc(iz, g.nz));
   L.p[F_EX][to] = L.p[F_EX][from];
   L.p[F_EY][to] = L.p[F_EY][from];
   L.p[F_EZ][to] = L.p[F_EZ][from];
@@ -437,7 +441,7 @@ void launch_unload_advance_e(Context& c, bool unload, bool advance_e) {
 
 void launch_ghost_sync(Context& c) {
   const GridC& g = c.gc;
-  const long long n = 2LL * g.pny * g.pnz + 2LL * g.pnx * g.pnz + 2LL * g.pnx * g.pny;
+  const long long n = 2LL * g.pny * g.pnz + 2LL * g.pnx * g.pnz + 2LL * g.pnx * g.pny;  // >= the faces synced
   ghost_sync_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(g, lanes_of(c));
   c.count_launch();
 }
@@ -445,14 +449,27 @@ void launch_ghost_sync(Context& c) {
 void launch_ghost_fold(Context& c) {
   const GridC& g = c.gc;
   const long long nx = (long long)g.pny * g.pnz, ny = (long long)g.nx * g.pnz, nz = (long long)g.nx * g.ny;
-  // x-decomposed: the x planes were folded into the neighbours by exchange
-  if (!g.xopen) {
+  // x -> y -> z; a walled axis folds its mirror images / drops (boundary.cu);
+  // x-decomposed: the shared x planes were folded into the neighbours by
+  // exchange (a global x wall is folded here)
+  if (g.xopen) {
+    if (g.wall_p[0] || g.wall_p[1]) launch_wall_fold(c, 0);
+  } else {
     fold_x_kernel<<<(unsigned)((nx + 255) / 256), 256, 0, c.stream>>>(g, c.acc);
     c.count_launch();
   }
-  fold_y_kernel<<<(unsigned)((ny + 255) / 256), 256, 0, c.stream>>>(g, c.acc);
-  fold_z_kernel<<<(unsigned)((nz + 255) / 256), 256, 0, c.stream>>>(g, c.acc);
-  c.count_launch(2);
+  if (g.ywall) {
+    launch_wall_fold(c, 1);
+  } else {
+    fold_y_kernel<<<(unsigned)((ny + 255) / 256), 256, 0, c.stream>>>(g, c.acc);
+    c.count_launch();
+  }
+  if (g.zwall) {
+    launch_wall_fold(c, 2);
+  } else {
+    fold_z_kernel<<<(unsigned)((nz + 255) / 256), 256, 0, c.stream>>>(g, c.acc);
+    c.count_launch();
+  }
 }
 
 void launch_clear_currents(Context& c) {

@@ -39,10 +39,12 @@ struct GridC {
   // x_low_wraps: this slab's low face is the global periodic boundary
   // (rank 0), which fixes the summation order of the wrapped unload edge.
   int xopen, x_low_wraps;
-  // Non-periodic x walls (pic_set_x_boundary; xopen is set too): particle
-  // bc per side (PIC_PBC_*; 0 = exchange with a neighbour when decomposed)
-  // and field bc (PIC_FBC_*).
-  int wall_p[2], wall_f[2];
+  // Non-periodic walls (pic_set_boundary), per face 2 axis + side (x low,
+  // x high, y low, ...): particle bc (PIC_PBC_*; on an x face 0 = exchange
+  // with a neighbour when decomposed) and field bc (PIC_FBC_*).  An x wall
+  // sets xopen; ywall / zwall: that axis has walls (both faces).
+  int wall_p[6], wall_f[6];
+  int ywall, zwall;
 };
 
 __device__ __forceinline__ unsigned fast_div(unsigned v, unsigned long long m) {

@@ -176,9 +176,11 @@ void ensure_mig_lists(Context& c, Species& s);
 // boundary.cu
 bool has_walls(const Context& c);
 void set_x_boundary(Context& c, int side, int pbc, int fbc);
+void set_boundary(Context& c, int face, int pbc, int fbc);
+bool absorbing_walls(const Context& c);
 void check_walls(const Context& c, bool deterministic);
 void absorb_compact(Context& c, Species& s);
-void launch_wall_fold(Context& c);
+void launch_wall_fold(Context& c, int axis);
 void launch_wall_e_save(Context& c);
 void launch_wall_e(Context& c);
 void launch_wall_b(Context& c, float frac);

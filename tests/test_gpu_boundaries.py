@@ -320,3 +320,131 @@ def test_decomposed_walls_particles(pbc):
         exp_p[3, m] = -want_p[3, m]
         assert (gids == exp_ids).all()
         assert (gp.view(np.uint32) == exp_p.view(np.uint32)).all()
+
+
+# ------------------------------------------------------------------ y / z walls
+def _ballistic_axis(g, n, seed, axis):
+    """Ballistic particles moving mostly along `axis` (see _ballistic_state)."""
+    p, ids = _ballistic_state(g, n, seed)
+    p[[3, 3 + axis]] = p[[3 + axis, 3]]
+    return p, ids
+
+
+def _periodic_reference_axis(g, p, ids, steps, axis):
+    from oracle.bindings import Orc
+    orc = Orc()
+    og = _og(g)
+    state = [(Q, M, p.copy(), ids.copy())]
+    f = np.zeros((16, g.padded), np.float32)
+    n = (g.nx, g.ny, g.nz)[axis]
+    pitch = (1, g.nx + 2, (g.nx + 2) * (g.ny + 2))[axis]
+    size = (g.nx + 2, g.ny + 2, g.nz + 2)[axis]
+    coord = lambda i: (i // pitch) % size  # noqa: E731
+    wraps = np.zeros(ids.size, np.int64)
+    for _ in range(steps):
+        c0 = coord(state[0][3])
+        orc.step(og, state, f)
+        c1 = coord(state[0][3])
+        wraps += ((c0 == n) & (c1 == 1)).astype(np.int64) - ((c0 == 1) & (c1 == n)).astype(np.int64)
+    return state[0][2], state[0][3], wraps
+
+
+@pytest.mark.parametrize("axis", [1, 2])
+@pytest.mark.parametrize("pbc", [PBC_REFLECT, PBC_ABSORB])
+def test_yz_walls_exact(axis, pbc):
+    """Walls on the y or z faces: reflection is the bit-exact mirror of the
+    periodic run along that axis, absorption removes exactly the leavers."""
+    import paper_2102_13133_b200 as pic
+    g = pic.make_grid((4, 6, 5) if axis == 1 else (4, 3, 6), 1.0, dt=0.25)
+    p, ids = _ballistic_axis(g, 3000, seed=7 + axis, axis=axis)
+    steps = 16
+    want_p, want_ids, wraps = _periodic_reference_axis(g, p, ids, steps, axis)
+    assert (np.abs(wraps) <= 1).all() and (wraps != 0).sum() > 50
+    with pic.Context(g) as ctx:
+        fbc = FBC_PEC if pbc == PBC_REFLECT else FBC_MUR
+        ctx.set_boundary(2 * axis, pbc, fbc)
+        ctx.set_boundary(2 * axis + 1, pbc, fbc)
+        sid = ctx.add_species("e", Q, M, ids.size)
+        ctx.upload_species(sid, p, ids)
+        for _ in range(steps):
+            ctx.step()
+        if pbc == PBC_ABSORB:
+            lo, hi = ctx.absorbed_counts()
+        gp, gids = ctx.download_species(sid)
+    gp, gids = _by_tag(gp, gids)
+    if pbc == PBC_ABSORB:
+        keep = wraps == 0
+        assert (lo, hi) == (int((wraps == -1).sum()), int((wraps == 1).sum()))
+        assert (gids == want_ids[keep]).all()
+        assert (gp.view(np.uint32) == want_p[:, keep].view(np.uint32)).all()
+        return
+    n = (g.nx, g.ny, g.nz)[axis]
+    pitch = (1, g.nx + 2, (g.nx + 2) * (g.ny + 2))[axis]
+    c = (want_ids // pitch) % (n + 2)
+    exp_ids = np.where(wraps != 0, want_ids + (n + 1 - 2 * c) * pitch, want_ids).astype(np.int32)
+    exp_p = want_p.copy()
+    m = wraps != 0
+    exp_p[axis, m] = -want_p[axis, m]
+    exp_p[3 + axis, m] = -want_p[3 + axis, m]
+    assert (gids == exp_ids).all()
+    assert (gp.view(np.uint32) == exp_p.view(np.uint32)).all()
+
+
+def test_closed_box_conserves_charge_and_particles():
+    """Reflecting conductor walls on all six faces around a thermal e/i
+    plasma: no particle is lost and div E - rho stays fixed at every node off
+    the wall planes."""
+    import paper_2102_13133_b200 as pic
+    g = pic.make_grid((10, 8, 7), 1.0, dt=0.25)
+    with pic.Context(g) as ctx:
+        for face in range(6):
+            ctx.set_boundary(face, PBC_REFLECT, FBC_PEC)
+        e = ctx.add_species("e", -1.0 / 16, 1.0 / 16, 16 * g.interior)
+        i = ctx.add_species("i", 1.0 / 16, 25.0 / 16, 16 * g.interior)
+        ctx.load_synthetic(e, 16, 0.3, seed=3)
+        ctx.load_synthetic(i, 16, 0.05, seed=4)
+
+        def residual():
+            ctx.refresh_charge_diagnostics()
+            r = ctx.download_fields()[F["div_e_err"]].reshape(g.nz + 2, g.ny + 2, g.nx + 2)
+            return r[2:g.nz + 1, 2:g.ny + 1, 2:g.nx + 1].astype(np.float64)  # off the wall planes
+
+        r0 = residual()
+        for _ in range(60):
+            ctx.step()
+        r1 = residual()
+        n = ctx.species_count(e) + ctx.species_count(i)
+    assert n == 32 * g.interior
+    assert np.abs(r1 - r0).max() <= 1e-4 * np.abs(r0).max(), np.abs(r1 - r0).max() / np.abs(r0).max()
+
+
+@pytest.mark.parametrize("fbc", [FBC_PEC, FBC_MUR])
+def test_pulse_along_y(fbc):
+    """An E_z / B_x pulse travelling +y: PEC y walls reflect it with its
+    energy, Mur y walls let it out."""
+    import paper_2102_13133_b200 as pic
+    g = pic.make_grid((2, 160, 2), 1.0, dt=0.5)
+    f = np.zeros((16, g.padded), np.float32)
+    ez = f[F["ez"]].reshape(g.nz + 2, g.ny + 2, g.nx + 2)
+    bx = f[F["cbx"]].reshape(g.nz + 2, g.ny + 2, g.nx + 2)
+    ye = (np.arange(g.ny + 2) - 1) * g.hy          # E_z on y node planes
+    yb = (np.arange(g.ny + 2) - 0.5) * g.hy        # B_x at y cell centres
+    ez[:] = (1e-2 * np.exp(-((ye - 100.0) / 6.0) ** 2))[None, :, None]
+    bx[:] = (1e-2 * np.exp(-((yb - 100.0) / 6.0) ** 2))[None, :, None]  # +y: E x B = E_z z x B_x x = +y
+    ez[:, 0, :] = 0
+    bx[:, 0, :] = 0
+    with pic.Context(g) as ctx:
+        ctx.set_boundary(2, PBC_ABSORB, fbc)
+        ctx.set_boundary(3, PBC_ABSORB, fbc)
+        ctx.upload_fields(f)
+        e0 = sum(ctx.field_energy())
+        for _ in range(200):
+            ctx.step()
+        e1 = sum(ctx.field_energy())
+        ezf = ctx.download_fields()[F["ez"]].reshape(g.nz + 2, g.ny + 2, g.nx + 2)[1, 1:-1, 1]
+    if fbc == FBC_PEC:
+        assert abs(e1 - e0) <= 0.02 * e0, (e0, e1)
+        k = int(np.argmax(np.abs(ezf)))
+        assert 105 <= k <= 135 and ezf[k] < 0, (k, ezf[k])
+    else:
+        assert e1 <= 0.02 * e0, (e0, e1)
