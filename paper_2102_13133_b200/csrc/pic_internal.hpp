@@ -74,10 +74,13 @@ struct Context {
   int* h_err = nullptr;       // pinned
   std::vector<Species> species;
   uint64_t launches = 0;
-  // advance_p strategy (push.cu): 30 = run-per-lane, TMA in/out, 2 voxel slots holding
-  // first-segment moments (default); 20 = the same with per-particle weights;
-  // 7 = TMA-staged CTA rounds with warp reduction;
-  // 0 = one particle per thread; 1, 5, 6, 8, 9 = TMA-staged ablations; 2-4 = other ablations
+  // advance_p strategy (push.cu): 52 = advance_p_lean (run-per-lane, TMA in /
+  // out, two voxel slots of first-segment moments, call-free IEEE loop body,
+  // index-only crosser queue; the default); 43 = the same with the full queue;
+  // 42 = advance_p_run capped at 85 registers (exact_gyration and
+  // out-of-range decks use it); 30 / 20 = earlier run-per-lane forms;
+  // 7 = TMA-staged CTA rounds with warp reduction; 0 = one particle per
+  // thread; the rest are measured ablations, 99 a timing probe
   int push_variant = 52;
   // sort_particles (blocked): 0 = LSD radix over (voxel, index), 1 = tiled counting sort (ablation)
   int sort_variant = 0;
