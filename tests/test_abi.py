@@ -45,7 +45,7 @@ def test_kernels_are_the_cuda_path():
     accumulator, no local-memory traffic; the sort ranks with MATCH."""
     sass = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
     funcs = re.split(r"\n\s+Function : ", sass)
-    push = [f for f in funcs if f.startswith("_ZN4picb14advance_p_leanILi8ELi6ELb0ELb0ELb0ELi4ELi0ELb0ELb1E")]
+    push = [f for f in funcs if f.startswith("_ZN4picb14advance_p_leanILi8ELi6ELb0ELb0ELi0ELi4ELi0ELb0ELb1E")]
     assert push, "default advance_p kernel not found"
     body = push[0]
     assert "REDG.E.ADD.F32x4" in body

@@ -14,6 +14,9 @@ from bench import CONFIGS  # noqa: E402
 cfg_name = sys.argv[1] if len(sys.argv) > 1 else "two_stream"
 variants = [int(v) for v in sys.argv[2].split(",")] if len(sys.argv) > 2 else [2, 3, 10, 11, 12]
 stales = [int(v) for v in sys.argv[3].split(",")] if len(sys.argv) > 3 else [0, 10]
+# "resort": sort the stores after the stale steps (run with PIC_SORT_DEFER=0),
+# so the timed steps see a fresh order at a later physical time
+resort = len(sys.argv) > 4 and sys.argv[4] == "resort"
 cfg = CONFIGS[cfg_name]
 g = pic.make_grid(cfg["n"], cfg["h"], dt=cfg["dt"])
 ctx = pic.Context(g)
@@ -29,6 +32,9 @@ for stale in stales:
         ctx._set_push_variant(2)
         for _ in range(stale):
             ctx.step()
+        if resort:
+            for sid in sids:
+                ctx.sort_particles(sid)
         ctx._set_push_variant(var)
         ctx.phase_timing(True)
         ctx.phase_timings(reset=True)
