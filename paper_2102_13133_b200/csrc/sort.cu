@@ -201,8 +201,11 @@ radix_hist_kernel(const unsigned* __restrict__ keys, const float4* __restrict__ 
 // digit.  VALS: 0 = the value is the key's index (first pass), 1 = load vals.
 // GATHER: instead of (key, value) pairs write the 32-byte particle record
 // the value indexes (the permute fused into the last pass).
+// The first pass (values = indices) runs 4 CTAs per SM at 64 registers (a
+// few spilled words): its loads are latency-bound, 3.20 vs 3.76 ms per 2^29
+// keys; the later passes gain nothing from it (2.77 vs 2.82 ms) and keep 3.
 template <int BITS, int VALS, bool GATHER, bool MATCH>
-__global__ void __launch_bounds__(kThreads, 3)
+__global__ void __launch_bounds__(kThreads, VALS == 0 ? 4 : 3)
 radix_scatter_kernel(const unsigned* __restrict__ keys, const unsigned* __restrict__ vals, size_t n, int shift,
                      size_t ntiles, const unsigned* __restrict__ offsets, unsigned* __restrict__ keys_out,
                      unsigned* __restrict__ vals_out, const float4* __restrict__ pos,
