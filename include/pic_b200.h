@@ -91,7 +91,8 @@ int pic_species_download(pic_context* ctx, int species, float* lanes7,
                          int32_t* ids);
 /* Native-record upload/download: two float4 streams per particle,
  * pos = (dx, dy, dz, bits(id)) and mom = (ux, uy, uz, w) — the 32-byte
- * device record, no layout conversion. */
+ * device record, no layout conversion.  The pointers may be host or device
+ * memory (unified addressing: device-to-device copies stay on the GPU). */
 int pic_species_upload_records(pic_context* ctx, int species, size_t n,
                                const void* pos16, const void* mom16);
 int pic_species_download_records(pic_context* ctx, int species, void* pos16,

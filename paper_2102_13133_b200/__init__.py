@@ -293,15 +293,23 @@ class Context:
         check(lib().pic_species_download(self._h, sid, p, ids))
         return p, ids
 
-    def upload_records(self, sid: int, pos16: np.ndarray, mom16: np.ndarray, n: int):
-        """Native 32-byte records: pos/mom float32 arrays of shape (>= n, 4)."""
-        assert pos16.dtype == np.float32 and mom16.dtype == np.float32 and pos16.shape[0] >= n
-        check(lib().pic_species_upload_records(self._h, sid, n, pos16.ctypes.data, mom16.ctypes.data))
+    @staticmethod
+    def _addr(a):
+        """Address of a numpy array or a (host or CUDA) torch tensor."""
+        return a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data
 
-    def download_records(self, sid: int, pos16: np.ndarray, mom16: np.ndarray) -> int:
+    def upload_records(self, sid: int, pos16, mom16, n: int):
+        """Native 32-byte records: pos/mom float32 arrays of shape (>= n, 4),
+        numpy or torch (host or CUDA: device copies stay on the GPU)."""
+        for a in (pos16, mom16):
+            assert str(a.dtype).endswith("float32") and a.shape[0] >= n and a.shape[1] == 4
+        check(lib().pic_species_upload_records(self._h, sid, n, self._addr(pos16), self._addr(mom16)))
+
+    def download_records(self, sid: int, pos16, mom16) -> int:
         n = self.species_count(sid)
-        assert pos16.shape[0] >= n and mom16.shape[0] >= n
-        check(lib().pic_species_download_records(self._h, sid, pos16.ctypes.data, mom16.ctypes.data))
+        for a in (pos16, mom16):
+            assert str(a.dtype).endswith("float32") and a.shape[0] >= n and a.shape[1] == 4
+        check(lib().pic_species_download_records(self._h, sid, self._addr(pos16), self._addr(mom16)))
         return n
 
     def load_synthetic(self, sid: int, ppc: int, u_th: float, drift=(0.0, 0.0, 0.0), seed: int = 1):

@@ -518,8 +518,8 @@ int pic_species_upload_records(pic_context* ctx, int species, size_t n, const vo
     if (n > s.cap) throw UsageError("species upload: count exceeds capacity");
     s.n = n;
     if (n == 0) return;
-    CUDA_OK(cudaMemcpyAsync(s.pos, pos16, n * 16, cudaMemcpyHostToDevice, c.stream));
-    CUDA_OK(cudaMemcpyAsync(s.mom, mom16, n * 16, cudaMemcpyHostToDevice, c.stream));
+    CUDA_OK(cudaMemcpyAsync(s.pos, pos16, n * 16, cudaMemcpyDefault, c.stream));
+    CUDA_OK(cudaMemcpyAsync(s.mom, mom16, n * 16, cudaMemcpyDefault, c.stream));
     CUDA_OK(cudaStreamSynchronize(c.stream));
   });
 }
@@ -530,8 +530,8 @@ int pic_species_download_records(pic_context* ctx, int species, void* pos16, voi
     Species& s = species_at(c, species);
     quiesce(c);
     if (s.n == 0) return;
-    CUDA_OK(cudaMemcpyAsync(pos16, s.pos, s.n * 16, cudaMemcpyDeviceToHost, c.stream));
-    CUDA_OK(cudaMemcpyAsync(mom16, s.mom, s.n * 16, cudaMemcpyDeviceToHost, c.stream));
+    CUDA_OK(cudaMemcpyAsync(pos16, s.pos, s.n * 16, cudaMemcpyDefault, c.stream));
+    CUDA_OK(cudaMemcpyAsync(mom16, s.mom, s.n * 16, cudaMemcpyDefault, c.stream));
     CUDA_OK(cudaStreamSynchronize(c.stream));
   });
 }
