@@ -30,8 +30,11 @@ void* Context::scratch_bytes(int slot, size_t bytes) {
       scratch[slot] = nullptr;
       scratch_size[slot] = 0;
     }
-    CUDA_OK(cudaMalloc(&scratch[slot], bytes));
-    scratch_size[slot] = bytes;
+    // slack for slots whose size varies step to step (segments, movers):
+    // a new maximum by a few percent must not free and reallocate tens of GB
+    const size_t want = ((bytes + bytes / 8) + (2u << 20) - 1) / (2u << 20) * (2u << 20);
+    CUDA_OK(cudaMalloc(&scratch[slot], want));
+    scratch_size[slot] = want;
   }
   return scratch[slot];
 }

@@ -215,6 +215,8 @@ float kinetic_energy(Context& c, Species& s, bool centered);  // synchronous
 // ---- sort / scan primitives --------------------------------------------------
 int key_bits_for(long long max_key_exclusive);
 void exclusive_scan_u32(Context& c, const unsigned* in, unsigned* out, size_t n);
+// start[v] = first position of key v in the sorted keys, start[V] = n
+void key_run_starts(Context& c, const unsigned* skey, size_t n, size_t V, unsigned* start);
 // Stable LSD radix sort of (key, value) pairs on the context stream.  vals ==
 // nullptr means values are the identity 0..n-1.  Results are in
 // *keys_out / *vals_out (scratch buffers owned by the context).

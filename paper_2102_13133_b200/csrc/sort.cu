@@ -557,6 +557,16 @@ static void scan_level(Context& c, const unsigned* in, unsigned* out, size_t n, 
   c.count_launch();
 }
 
+// start[v] = first position of key v in a sorted key array (start[V] = n).
+void key_run_starts(Context& c, const unsigned* skey, size_t n, size_t V, unsigned* start) {
+  CUDA_OK(cudaMemsetAsync(start, 0, (V + 1) * 4, c.stream));
+  if (n) {
+    count_keys_kernel<<<blocks_for(n), 256, 0, c.stream>>>(skey, n, start);
+    c.count_launch();
+  }
+  exclusive_scan_u32(c, start, start, V + 1);
+}
+
 void exclusive_scan_u32(Context& c, const unsigned* in, unsigned* out, size_t n) {
   if (n == 0) return;
   // partial sums of every level live back to back in one grow-only slot
