@@ -370,46 +370,55 @@ class DecomposedSim:
         self.transport.exchange(msgs)
 
     # --- the three exchanges ----------------------------------------------------
-    def migrate(self, sid):
+    def migrate(self, sids=None):
+        """Particle migration after the pushes, every species in one round:
+        one count exchange (one host read-back) and one payload exchange
+        for all species, then the appends in species order."""
         g = self.geom
-        counts = {r: e.migrate_counts(sid) for r, e in self.slabs.items()}
-        # 1) counts
+        sids = list(range(self.nspecies)) if sids is None else list(sids)
+        if not sids:
+            return
+        counts = {r: [e.migrate_counts(sid) for sid in sids] for r, e in self.slabs.items()}
+        # 1) counts: one message per direction holding every species' count
         sends, recvs = [], []
         for r, e in self.slabs.items():
             for d in (DOWN, UP):
                 dst = g.low(r) if d == DOWN else g.high(r)
                 if g.crosses_wall(r, d):  # particles leaving through an absorbing wall
-                    self.absorbed[d] += counts[r][d]
+                    self.absorbed[d] += sum(c[d] for c in counts[r])
                 else:
-                    sends.append((r, dst, d, e.count_buffer([counts[r][d]]), None))
+                    sends.append((r, dst, d, e.count_buffer([c[d] for c in counts[r]]), None))
                 src = g.high(r) if d == DOWN else g.low(r)
                 if not g.crosses_wall(src, d):
-                    recvs.append((src, r, d, e.count_buffer([0])))
+                    recvs.append((src, r, d, e.count_buffer([0] * len(sids))))
         self._run(sends, recvs)
-        incoming = {(r, d): 0 for r in self.slabs for d in (DOWN, UP)}
+        incoming = {(r, d, k): 0 for r in self.slabs for d in (DOWN, UP) for k in range(len(sids))}
         for src, r, d, buf in recvs:
-            incoming[(r, d)] = self.slabs[r].read_counts(buf)[0]
+            for k, c in enumerate(self.slabs[r].read_counts(buf)):
+                incoming[(r, d, k)] = c
         # 2) payloads (32 B records), packed while the stores compact
         sends, recvs = [], []
-        for r, e in self.slabs.items():
-            lo = self._buf(r, ("mig", "s", DOWN), 32 * counts[r][DOWN])
-            hi = self._buf(r, ("mig", "s", UP), 32 * counts[r][UP])
-            e.migrate_pack(sid, lo, hi)  # a wall side's buffer is packed and dropped
-            if not g.crosses_wall(r, DOWN):
-                sends.append((r, g.low(r), DOWN, lo, None))
-            if not g.crosses_wall(r, UP):
-                sends.append((r, g.high(r), UP, hi, None))
-            for d in (DOWN, UP):
-                src = g.high(r) if d == DOWN else g.low(r)
-                if not g.crosses_wall(src, d):
-                    recvs.append((src, r, d, self._buf(r, ("mig", "r", d), 32 * incoming[(r, d)])))
+        for k, sid in enumerate(sids):
+            for r, e in self.slabs.items():
+                lo = self._buf(r, ("mig", sid, "s", DOWN), 32 * counts[r][k][DOWN])
+                hi = self._buf(r, ("mig", sid, "s", UP), 32 * counts[r][k][UP])
+                e.migrate_pack(sid, lo, hi)  # a wall side's buffer is packed and dropped
+                if not g.crosses_wall(r, DOWN):
+                    sends.append((r, g.low(r), (DOWN, k), lo, None))
+                if not g.crosses_wall(r, UP):
+                    sends.append((r, g.high(r), (UP, k), hi, None))
+                for d in (DOWN, UP):
+                    src = g.high(r) if d == DOWN else g.low(r)
+                    if not g.crosses_wall(src, d):
+                        recvs.append((src, r, (d, k), self._buf(r, ("mig", sid, "r", d), 32 * incoming[(r, d, k)])))
         self._run(sends, recvs)
         # 3) append: from the low neighbour (UP messages) first, then the high
-        for r, e in self.slabs.items():
-            for d in (UP, DOWN):
-                n = incoming[(r, d)]
-                if n:
-                    e.migrate_append(sid, self._buf(r, ("mig", "r", d), 32 * n), n)
+        for k, sid in enumerate(sids):
+            for r, e in self.slabs.items():
+                for d in (UP, DOWN):
+                    n = incoming[(r, d, k)]
+                    if n:
+                        e.migrate_append(sid, self._buf(r, ("mig", sid, "r", d), 32 * n), n)
 
     def fold_accumulator(self):
         """x halo-add: ghost plane 0 -> low neighbour's plane nx, ghost nx+1 ->
@@ -442,8 +451,7 @@ class DecomposedSim:
             for sid in range(self.nspecies):
                 e.advance_p(sid, flags)
             mark("push", False)
-        for sid in range(self.nspecies):
-            self.migrate(sid)
+        self.migrate()
         for e in self.slabs.values():
             self._wall(e, STAGE_EMIT)
         self.fold_accumulator()
