@@ -451,9 +451,10 @@ class DecomposedSim:
             for sid in range(self.nspecies):
                 e.advance_p(sid, flags)
             mark("push", False)
-        self.migrate()
-        for e in self.slabs.values():
-            self._wall(e, STAGE_EMIT)
+        # the field half of the step needs only the accumulator, the
+        # migration only the particle stores: the fields go first so the
+        # migration's count read-back (a host sync) comes after all of the
+        # step's device work has been queued
         self.fold_accumulator()
         for e in self.slabs.values():
             e.advance_b(0.5)
@@ -468,6 +469,9 @@ class DecomposedSim:
             e.advance_b(0.5)
             self._wall(e, STAGE_AFTER_B, 0.5)
         self.sync_fields()
+        self.migrate()
+        for e in self.slabs.values():
+            self._wall(e, STAGE_EMIT)
 
     def set_laser(self, ix_global: int, e0: float, omega: float, **kw):
         """The laser plane (global node index) on the slab that owns it."""
