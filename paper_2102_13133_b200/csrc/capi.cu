@@ -112,6 +112,13 @@ void Context::release() {
   if (cs_in) cudaStreamDestroy(cs_in);
   if (cs_out) cudaStreamDestroy(cs_out);
   cs_in = cs_out = nullptr;
+  for (int k = 0; k < kSide; ++k) {
+    if (side[k]) cudaStreamDestroy(side[k]);
+    if (fork_ev[k]) cudaEventDestroy(fork_ev[k]);
+    if (join_ev[k]) cudaEventDestroy(join_ev[k]);
+    side[k] = nullptr;
+    fork_ev[k] = join_ev[k] = nullptr;
+  }
   if (own_stream) stream = own_stream;  // never destroy a borrowed stream
   if (stream) cudaStreamDestroy(stream);
   f = nullptr;
@@ -159,6 +166,7 @@ Context* make_context(int device, const pic_grid& g) {
     CUDA_OK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CUDA_OK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     if (const char* v = std::getenv("PIC_PUSH_VARIANT")) c->push_variant = std::atoi(v);  // profiling knob
+    if (const char* v = std::getenv("PIC_FORK_SPECIES")) c->fork_species = std::atoi(v) != 0;  // profiling knob
     if (const char* v = std::getenv("PIC_SORT_VARIANT")) set_sort_variant(*c, std::atoi(v));  // profiling knob
     if (const char* v = std::getenv("PIC_SORT_DEFER")) c->sort_defer = std::atoi(v) != 0;     // profiling knob
     if (const char* v = std::getenv("PIC_HOST_BUFS")) c->host_bufs = std::atoi(v);            // profiling knob
@@ -264,12 +272,42 @@ void step(Context& c, unsigned flags) {
   check_walls(c, det);
   step_prologue(c);
   c.phase_begin(Context::kPhPush);
-  for (auto& s : c.species) {
-    if (det)
+  // fast mode without walls: species 1.. on side streams (fork / join; also
+  // inside a graph capture), so the small decks' pushes overlap their tails
+  const size_t ns = c.species.size();
+  const bool fork = !det && !walls && c.fork_species && ns > 1;
+  if (fork && !c.side[0]) {
+    for (int k = 0; k < Context::kSide; ++k) {
+      CUDA_OK(cudaStreamCreateWithFlags(&c.side[k], cudaStreamNonBlocking));
+      CUDA_OK(cudaEventCreateWithFlags(&c.fork_ev[k], cudaEventDisableTiming));
+      CUDA_OK(cudaEventCreateWithFlags(&c.join_ev[k], cudaEventDisableTiming));
+    }
+  }
+  const size_t nside = fork ? std::min<size_t>(ns - 1, Context::kSide) : 0;
+  if (nside) CUDA_OK(cudaEventRecord(c.fork_ev[0], c.stream));
+  for (size_t k = 0; k < nside; ++k) CUDA_OK(cudaStreamWaitEvent(c.side[k], c.fork_ev[0], 0));
+  for (size_t i = 0; i < ns; ++i) {
+    Species& s = c.species[i];
+    if (det) {
       launch_advance_p_deterministic(c, s, exact);
-    else
+    } else if (nside && i > 0) {
+      cudaStream_t main = c.stream;
+      c.stream = c.side[(i - 1) % nside];
+      try {
+        launch_advance_p(c, s, exact);
+      } catch (...) {
+        c.stream = main;
+        throw;
+      }
+      c.stream = main;
+    } else {
       launch_advance_p(c, s, exact);
+    }
     if (walls && absorbing_walls(c)) absorb_compact(c, s);
+  }
+  for (size_t k = 0; k < nside; ++k) {
+    CUDA_OK(cudaEventRecord(c.join_ev[k], c.side[k]));
+    CUDA_OK(cudaStreamWaitEvent(c.stream, c.join_ev[k], 0));
   }
   wall_stage(c, PIC_STAGE_EMIT, 0.f);
   c.phase_end();

@@ -110,6 +110,13 @@ struct Context {
   std::vector<uint64_t> graph_seen;
   bool use_graphs = true;
   cudaEvent_t events[64] = {};
+  // fast-mode step: species after the first push on side streams (their
+  // CTAs fill the first push's tail; the pushes share only the atomically
+  // updated accumulator)
+  static constexpr int kSide = 3;
+  bool fork_species = true;
+  cudaStream_t side[kSide] = {};
+  cudaEvent_t fork_ev[kSide] = {}, join_ev[kSide] = {};
 
   enum ScratchSlot {
     kScrStage = 0, kScrNseg, kScrOff, kScrSegKey, kScrSegW,
