@@ -109,6 +109,32 @@ load_interpolators_kernel(GridC g, Lanes L, float4* __restrict__ out) {
   }
 }
 
+// Periodic ghost images of one interior voxel's three lanes: every ghost
+// voxel whose wrapped image is (ix, iy, iz) — what ghost_sync_kernel would
+// copy there (fully periodic boxes only).  Interior cells off the faces
+// have none.
+__device__ __forceinline__ void write_ghost_images(const GridC& g, int ix, int iy, int iz, float* a, float* b,
+                                                   float* c, float va, float vb, float vc) {
+  if (ix != 1 && ix != g.nx && iy != 1 && iy != g.ny && iz != 1 && iz != g.nz) return;
+  int lx[3], ly[3], lz[3], nxl = 1, nyl = 1, nzl = 1;
+  lx[0] = ix; ly[0] = iy; lz[0] = iz;
+  if (ix == g.nx) lx[nxl++] = 0;
+  if (ix == 1) lx[nxl++] = g.nx + 1;
+  if (iy == g.ny) ly[nyl++] = 0;
+  if (iy == 1) ly[nyl++] = g.ny + 1;
+  if (iz == g.nz) lz[nzl++] = 0;
+  if (iz == 1) lz[nzl++] = g.nz + 1;
+  for (int k = 0; k < nzl; ++k)
+    for (int j = 0; j < nyl; ++j)
+      for (int i = 0; i < nxl; ++i) {
+        if (i == 0 && j == 0 && k == 0) continue;
+        const size_t w = (size_t)voxel_of(g, lx[i], ly[j], lz[k]);
+        a[w] = va;
+        b[w] = vb;
+        c[w] = vc;
+      }
+}
+
 // ---- advance_b (fields.cpp:113-151) -----------------------------------------
 struct BCoef {
   float c1x, c2x, c1y, c2y, c1z, c2z;
@@ -117,6 +143,10 @@ struct BCoef {
 // every round issued before the first store: the one-voxel-per-thread form
 // stalled on load latency at half the DRAM bandwidth.
 constexpr int kBVox = 4;
+// kImages: the step's periodic ghost sync after this update is fused in
+// (B's ghost images written here; E's ghosts are unchanged since the last
+// sync)
+template <bool kImages>
 __global__ void __launch_bounds__(256)
 advance_b_kernel(GridC g, Lanes L, BCoef k) {
   const size_t sx = 1, sy = (size_t)g.sy, sz = (size_t)g.sz;
@@ -130,10 +160,14 @@ advance_b_kernel(GridC g, Lanes L, BCoef k) {
   size_t v[kBVox];
   bool ok[kBVox];
   float e0[kBVox][3], e1[kBVox][6], b0[kBVox][3];
+  int cx[kBVox], cy[kBVox], cz[kBVox];
 #pragma unroll
   for (int r = 0; r < kBVox; ++r) {
     int ix, iy, iz;
     ok[r] = interior_coords(g, base + r * 256, ix, iy, iz);
+    cx[r] = ix;
+    cy[r] = iy;
+    cz[r] = iz;
     v[r] = ok[r] ? (size_t)voxel_of(g, ix, iy, iz) : (size_t)g.sz + (size_t)g.sy + 1;  // a valid interior address
     const size_t w = v[r];
     e0[r][0] = ex[w]; e0[r][1] = ey[w]; e0[r][2] = ez[w];
@@ -146,9 +180,13 @@ advance_b_kernel(GridC g, Lanes L, BCoef k) {
     if (!ok[r]) continue;
     const size_t w = v[r];
     // dst = (dst + c1 * (p1 - p0)) + c2 * (q1 - q0)
-    bx[w] = (b0[r][0] + k.c1x * (e1[r][0] - e0[r][2])) + k.c2x * (e1[r][1] - e0[r][1]);
-    by[w] = (b0[r][1] + k.c1y * (e1[r][2] - e0[r][0])) + k.c2y * (e1[r][3] - e0[r][2]);
-    bz[w] = (b0[r][2] + k.c1z * (e1[r][4] - e0[r][1])) + k.c2z * (e1[r][5] - e0[r][0]);
+    const float nbx = (b0[r][0] + k.c1x * (e1[r][0] - e0[r][2])) + k.c2x * (e1[r][1] - e0[r][1]);
+    const float nby = (b0[r][1] + k.c1y * (e1[r][2] - e0[r][0])) + k.c2y * (e1[r][3] - e0[r][2]);
+    const float nbz = (b0[r][2] + k.c1z * (e1[r][4] - e0[r][1])) + k.c2z * (e1[r][5] - e0[r][0]);
+    bx[w] = nbx;
+    by[w] = nby;
+    bz[w] = nbz;
+    if (kImages) write_ghost_images(g, cx[r], cy[r], cz[r], bx, by, bz, nbx, nby, nbz);
   }
 }
 
@@ -177,7 +215,7 @@ __device__ __forceinline__ float gather4(float jf, float f, float v00, float v01
   return jf;
 }
 
-template <bool kUnload, bool kAdvanceE>
+template <bool kUnload, bool kAdvanceE, bool kImages = false>
 __global__ void __launch_bounds__(256)
 unload_advance_e_kernel(GridC g, Lanes L, const float* __restrict__ acc, ECoef k) {
   int ix, iy, iz;
@@ -218,9 +256,14 @@ unload_advance_e_kernel(GridC g, Lanes L, const float* __restrict__ acc, ECoef k
     const float* __restrict__ bz = L.p[F_BZ];
     const float bxv = bx[v], byv = by[v], bzv = bz[v];
     // dst = ((dst + c1 * (p1 - p0)) + c2 * (q1 - q0)) + c3 * r
-    L.p[F_EX][v] = ((L.p[F_EX][v] + k.c1x * (bzv - bz[v - sy])) + k.c2x * (byv - by[v - sz])) + k.c3 * jx;
-    L.p[F_EY][v] = ((L.p[F_EY][v] + k.c1y * (bxv - bx[v - sz])) + k.c2y * (bzv - bz[v - sx])) + k.c3 * jy;
-    L.p[F_EZ][v] = ((L.p[F_EZ][v] + k.c1z * (byv - by[v - sx])) + k.c2z * (bxv - bx[v - sy])) + k.c3 * jz;
+    const float nex = ((L.p[F_EX][v] + k.c1x * (bzv - bz[v - sy])) + k.c2x * (byv - by[v - sz])) + k.c3 * jx;
+    const float ney = ((L.p[F_EY][v] + k.c1y * (bxv - bx[v - sz])) + k.c2y * (bzv - bz[v - sx])) + k.c3 * jy;
+    const float nez = ((L.p[F_EZ][v] + k.c1z * (byv - by[v - sx])) + k.c2z * (bxv - bx[v - sy])) + k.c3 * jz;
+    L.p[F_EX][v] = nex;
+    L.p[F_EY][v] = ney;
+    L.p[F_EZ][v] = nez;
+    // the step's periodic ghost sync fused in: E's images (B's are current)
+    if (kImages) write_ghost_images(g, ix, iy, iz, L.p[F_EX], L.p[F_EY], L.p[F_EZ], nex, ney, nez);
   }
 }
 
@@ -403,7 +446,7 @@ void launch_load_interpolators(Context& c) {
   c.count_launch();
 }
 
-void launch_advance_b(Context& c, float frac) {
+void launch_advance_b(Context& c, float frac, bool images) {
   // constants computed on the host in real_t (fields.cpp:115-118, 133-138)
   const float fdt = frac * c.grid.dt;
   const float rhx = 1.0f / c.grid.hx, rhy = 1.0f / c.grid.hy, rhz = 1.0f / c.grid.hz;
@@ -411,11 +454,14 @@ void launch_advance_b(Context& c, float frac) {
   k.c1x = -fdt * rhy; k.c2x = fdt * rhz;
   k.c1y = -fdt * rhz; k.c2y = fdt * rhx;
   k.c1z = -fdt * rhx; k.c2z = fdt * rhy;
-  advance_b_kernel<<<interior_blocks(c.gc, 256 * kBVox), 256, 0, c.stream>>>(c.gc, lanes_of(c), k);
+  if (images)
+    advance_b_kernel<true><<<interior_blocks(c.gc, 256 * kBVox), 256, 0, c.stream>>>(c.gc, lanes_of(c), k);
+  else
+    advance_b_kernel<false><<<interior_blocks(c.gc, 256 * kBVox), 256, 0, c.stream>>>(c.gc, lanes_of(c), k);
   c.count_launch();
 }
 
-void launch_unload_advance_e(Context& c, bool unload, bool advance_e) {
+void launch_unload_advance_e(Context& c, bool unload, bool advance_e, bool images) {
   const float dt = c.grid.dt;
   const float rhx = 1.0f / c.grid.hx, rhy = 1.0f / c.grid.hy, rhz = 1.0f / c.grid.hz;
   ECoef k;
@@ -428,7 +474,9 @@ void launch_unload_advance_e(Context& c, bool unload, bool advance_e) {
   k.fy = c.grid.hy / two_dt_v;
   k.fz = c.grid.hz / two_dt_v;
   const unsigned b = interior_blocks(c.gc, 256);
-  if (unload && advance_e)
+  if (unload && advance_e && images)
+    unload_advance_e_kernel<true, true, true><<<b, 256, 0, c.stream>>>(c.gc, lanes_of(c), c.acc, k);
+  else if (unload && advance_e)
     unload_advance_e_kernel<true, true><<<b, 256, 0, c.stream>>>(c.gc, lanes_of(c), c.acc, k);
   else if (unload)
     unload_advance_e_kernel<true, false><<<b, 256, 0, c.stream>>>(c.gc, lanes_of(c), c.acc, k);

@@ -166,9 +166,10 @@ Species& species_at(Context& c, int sid);
 void launch_advance_p(Context& c, Species& s, bool exact_gyration);
 void launch_advance_p_deterministic(Context& c, Species& s, bool exact_gyration);
 void launch_load_interpolators(Context& c);
-void launch_advance_b(Context& c, float frac);
+// images: also write B's periodic ghost images (the step's fused ghost sync)
+void launch_advance_b(Context& c, float frac, bool images = false);
 // unload (jf += f_a * lane, gather form) and/or advance_e in one pass.
-void launch_unload_advance_e(Context& c, bool unload, bool advance_e);
+void launch_unload_advance_e(Context& c, bool unload, bool advance_e, bool images = false);
 void launch_ghost_sync(Context& c);
 void launch_ghost_fold(Context& c);
 void launch_clear_currents(Context& c);
