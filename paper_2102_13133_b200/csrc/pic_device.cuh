@@ -102,6 +102,16 @@ __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);
 }
+// A converged global load ahead of a divergent loop whose only earlier
+// global traffic is TMA: it makes ptxas keep the global memory descriptor
+// in a uniform register instead of re-materialising it (R2UR) before every
+// load and reduction of the loop.  Reads one L2-hot word; the OR of 0 never
+// changes the flag.
+__device__ __forceinline__ void pin_global_descriptor(const float4* __restrict__ p, int* __restrict__ flag) {
+  const float4 w = __ldg(p);
+  if (w.x == 1.2345e-38f && w.y == 3.25e-38f) atomicOr(flag, 0);
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
   asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
