@@ -94,6 +94,9 @@ def _lpi_config():
 CONFIGS["lpi"] = _lpi_config()
 
 BYTES_PER_PUSH = 64  # 32 B record read + 32 B record written
+# BASELINE.json's metric is per GPU; the line's value is the whole-job sum
+# over the N GPUs (the bench contract), value_per_gpu the BASELINE figure
+METRIC = "particle pushes/sec summed over all GPUs (advance_p, whole step); per GPU = value_per_gpu"
 
 
 def deck_text(cfg, n=None, workers=1, seed=4):
@@ -220,8 +223,14 @@ def profile_traffic():
 def cpu_reference(cfg_name, steps, warmup, sample_n=64, workers=None):
     """The reference CPU implementation (oracle/_ref: minipic compiled from its
     sources, fp32, AVX2 lane) on a bounded sample of the workload: the same
-    deck physics on a sample_n^3 box, all host cores.  Returns pushes/s for
-    the whole step with the sort amortised over sort_interval."""
+    deck physics on a sample_n^3 box, all host cores.  Times exactly `steps`
+    whole steps after `warmup` untimed ones, each step SimState::step plus the
+    run loop's sort cadence (sort_due_species, proj/src/sim.cpp:217-222,
+    285-305) — the same step our arm times.  When the timed steps contain no
+    sort point, one blocked sort of every species is timed separately and
+    amortised over sort_interval.  Also reports the reference bench harness's
+    own protocol (proj/src/bench.cpp:14,52-59: median of 3 after 1 warm-up)
+    over single steps.  Returns pushes/s."""
     from oracle.bindings import Ref, ref_available
 
     cfg = CONFIGS[cfg_name]
@@ -233,26 +242,35 @@ def cpu_reference(cfg_name, steps, warmup, sample_n=64, workers=None):
     sim = ref.sim(deck_text(cfg, n=n, workers=workers))
     npart = sum(sim.species(s)[1].size for s in range(sim.nspecies))
     for _ in range(warmup):
-        sim.step(1)
+        sim.step_and_sort(1)
     times = []
     for _ in range(steps):
         t0 = time.perf_counter()
-        sim.step(1)
+        sim.step_and_sort(1)
         times.append(time.perf_counter() - t0)
-    # amortised sort: one blocked sort of every species (serial in the
-    # reference, particles.cpp:412-458), divided by sort_interval
-    t0 = time.perf_counter()
-    for s in range(sim.nspecies):
-        p, ids = sim.species(s)
-        ref.sort(p, ids, interleaved=False)
-    t_sort = time.perf_counter() - t0
-    t_step = statistics.median(times) + t_sort / cfg["sort_interval"]
+    total = sum(times)
+    si = cfg["sort_interval"]
+    sorted_in_window = si > 0 and any((warmup + k + 1) % si == 0 for k in range(steps))
+    t_sort = 0.0
+    if si > 0 and not sorted_in_window:
+        t0 = time.perf_counter()
+        for s in range(sim.nspecies):
+            p, ids = sim.species(s)
+            ref.sort(p, ids, interleaved=False)
+        t_sort = time.perf_counter() - t0
+        total += t_sort * steps / si
+    med3 = statistics.median(times[:3]) if len(times) >= 3 else statistics.median(times)
     return {
-        "value": npart / t_step, "unit": "particle pushes/s", "cores": workers, "kind": "reference",
-        "sample": f"{cfg_name} deck physics on {n}^3 cells ({npart} particles), median of {steps} steps "
-                  f"after {warmup} warm-up, + blocked sort/{cfg['sort_interval']}; minipic fp32 AVX2, "
-                  f"{workers} workers",
-        "step_s": statistics.median(times), "sort_s": t_sort,
+        "value": npart * steps / total, "unit": "particle pushes/s", "cores": workers, "kind": "reference",
+        "sample": f"{cfg_name} deck physics on {n}^3 cells ({npart} particles): {steps} timed steps after "
+                  f"{warmup} warm-up, run-loop sort every {si}"
+                  + ("" if sorted_in_window or si <= 0 else f" (no sort point in the window: one blocked sort "
+                                                          f"timed, amortised /{si})")
+                  + f"; minipic fp32 AVX2, {workers} workers",
+        "steps": steps, "warmup": warmup, "ms_per_step": total / steps * 1e3, "sort_s": t_sort,
+        "particles": npart, "cells": n,
+        "bench_cpp_protocol": {"median_of_3_step_ms": med3 * 1e3,
+                               "note": "proj/src/bench.cpp:14,52-59: 1 warm-up, median of 3 timed repetitions"},
     }
 
 
@@ -505,7 +523,8 @@ def run_e2e_decomposed(pic, sim, ctx, sids, args, world):
     for h in host:
         pic.host_unregister(h[0])
         pic.host_unregister(h[1])
-    return {"value": float(tn.item()) * k / dt, "unit": "particle pushes/s", "h2d_bytes_per_step": byt // k,
+    return {"value": float(tn.item()) * k / dt, "value_per_gpu": float(tn.item()) * k / dt / world,
+            "unit": "particle pushes/s", "h2d_bytes_per_step": byt // k,
             "d2h_bytes_per_step": byt // k, "steps": k, "ms_per_step": dt / k * 1e3,
             "note": "per rank: records H2D, decomposed step, records D2H (not pipelined); bytes are rank 0's"}
 
@@ -539,7 +558,16 @@ def run_e2e(pic, ctx, sids, npart, args, world):
         pic.host_unregister(ids)
     b_in = sum(h[0].nbytes + h[1].nbytes for h in host)
     b_out = sum(h[0].nbytes * 6 // 7 + h[1].nbytes for h in host)  # lanes 0-5 + ids (w is not modified)
-    return {"value": npart * k * world / dt, "unit": "particle pushes/s", "h2d_bytes_per_step": b_in,
+    if world > 1:  # whole-job sum of every rank's particles
+        import torch
+        import torch.distributed as dist
+        tn = torch.tensor([float(npart)], dtype=torch.float64)
+        dist.all_reduce(tn)
+        npart_all = float(tn.item())
+    else:
+        npart_all = float(npart)
+    return {"value": npart_all * k / dt, "value_per_gpu": npart_all * k / dt / world,
+            "unit": "particle pushes/s", "h2d_bytes_per_step": b_in,
             "d2h_bytes_per_step": b_out, "steps": k, "ms_per_step": dt / k * 1e3}
 
 
@@ -585,18 +613,20 @@ def main():
             emit({"impl": "reference", "unavailable": f"the reference's deck text cannot express the "
                               f"{args.config} deck (built through the API here)"})
             return
-        r = cpu_reference(args.config, max(1, min(args.steps, 3)), max(1, min(args.warmup, 1)),
-                          sample_n=args.cpu_sample_n)
+        r = cpu_reference(args.config, max(1, args.steps), max(0, args.warmup), sample_n=args.cpu_sample_n)
         if r is None:
             emit({"impl": "reference", "unavailable": "oracle/_ref/libminipic_ref.so not built"})
             return
         line = {
-            "impl": "reference", "metric": "particle pushes/sec/GPU (advance_p, whole step)", "value": r["value"],
-            "unit": "particle pushes/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": r["step_s"] * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "impl": "reference", "metric": METRIC, "value": r["value"],
+            "unit": "particle pushes/s", "n_gpus": args.gpus, "steps": r["steps"], "warmup": r["warmup"],
+            "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic (reference Rng load)",
-            "config": {"workload": args.config, "cells": f"{cfg['n']}^3", "sample": r["sample"]},
+            "config": {"workload": args.config, "cells": f"{cfg['n']}^3", "sample_cells": f"{r['cells']}^3",
+                       "sample_particles": r["particles"], "same_config": r["cells"] == cfg["n"],
+                       "sample": r["sample"]},
             "cpu_baseline": {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "bench_cpp_protocol": r["bench_cpp_protocol"],
             "e2e": {"value": r["value"], "unit": "particle pushes/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
         }
@@ -631,7 +661,7 @@ def main():
         cpu = {"value": None, "note": "the reference cannot express this deck; see --config two_stream"}
     elif not args.no_cpu_baseline and world == 1:  # rank 0 at N=1 only
         try:
-            r = cpu_reference(args.config, 3, 1, sample_n=args.cpu_sample_n)
+            r = cpu_reference(args.config, 10, 1, sample_n=args.cpu_sample_n)
             if r:
                 cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as e:  # the baseline is reported, not required
@@ -639,8 +669,9 @@ def main():
     g = res["grid"]
     gl = res.get("local_grid", g)
     line = {
-        "metric": "particle pushes/sec/GPU (advance_p, whole step)",
+        "metric": METRIC,
         "value": value,
+        "value_per_gpu": value / world,
         "unit": "particle pushes/s",
         "n_gpus": world,
         "steps": args.steps,

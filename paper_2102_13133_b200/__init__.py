@@ -423,6 +423,16 @@ class Context:
         """SimState::step with host-resident species buffers (copied in and out)."""
         flags = (PIC_EXACT_GYRATION if exact_gyration else 0) | (PIC_DETERMINISTIC if deterministic else 0)
         k = len(lanes7_list)
+        ns = len(self.species_names)
+        if k != ns or len(ids_list) != ns:
+            raise UsageError(f"step_host: {k} lane arrays / {len(ids_list)} id arrays for {ns} species")
+        for s, (a, i) in enumerate(zip(lanes7_list, ids_list)):
+            n = self.species_count(s)
+            if not (isinstance(a, np.ndarray) and a.dtype == np.float32 and a.flags.c_contiguous
+                    and a.shape == (7, n)):
+                raise UsageError(f"step_host: species {s} lanes must be C-contiguous float32 (7, {n})")
+            if not (isinstance(i, np.ndarray) and i.dtype == np.int32 and i.flags.c_contiguous and i.shape == (n,)):
+                raise UsageError(f"step_host: species {s} ids must be C-contiguous int32 ({n},)")
         lp = (C.c_void_p * k)(*[a.ctypes.data for a in lanes7_list])
         ip = (C.c_void_p * k)(*[a.ctypes.data for a in ids_list])
         check(lib().pic_step_host(self._h, flags, lp, ip))

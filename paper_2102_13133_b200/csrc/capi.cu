@@ -165,7 +165,7 @@ Context* make_context(int device, const pic_grid& g) {
     CUDA_OK(cudaSetDevice(device));
     CUDA_OK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     CUDA_OK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
-    if (const char* v = std::getenv("PIC_PUSH_VARIANT")) c->push_variant = std::atoi(v);  // profiling knob
+    if (const char* v = std::getenv("PIC_PUSH_VARIANT")) set_push_variant(*c, std::atoi(v));  // profiling knob
     if (const char* v = std::getenv("PIC_FORK_SPECIES")) c->fork_species = std::atoi(v) != 0;  // profiling knob
     if (const char* v = std::getenv("PIC_SORT_VARIANT")) set_sort_variant(*c, std::atoi(v));  // profiling knob
     if (const char* v = std::getenv("PIC_SORT_DEFER")) c->sort_defer = std::atoi(v) != 0;     // profiling knob
@@ -210,6 +210,7 @@ void quiesce(Context& c) {
     if (e & kErrMover) msg += "advance_particles: mover failed to terminate; ";
     if (e & kErrWrap) msg += "wrap_periodic: displacement beyond one cell (CFL violation); ";
     if (e & kErrVoxel) msg += "coords_of: voxel id out of range; ";
+    if (e & kErrMigCap) msg += "advance_particles: emigrant / absorbed list overflow (raise the species capacity); ";
     throw RunAbort(msg);
   }
 }
@@ -433,8 +434,12 @@ int guard(Fn&& fn) {
 int picb::capi_guard(const std::function<void()>& fn) { return guard(fn); }
 
 namespace {
+// Every entry point runs on its context's device: contexts on several GPUs
+// may share one host thread (the scratch allocations, streams, events and
+// launches of a call all follow the current device).
 Context& C_(pic_context* p) {
   if (!p || !p->c) throw UsageError("null pic_context");
+  CUDA_OK(cudaSetDevice(p->c->device));
   return *p->c;
 }
 void check_launch() {
@@ -748,6 +753,9 @@ int pic_sort_particles(pic_context* ctx, int species, int order) {
 // the laser (host-computed amplitude), phase timing (host events).
 static bool graph_ok(const Context& c, unsigned flags) {
   if (flags & PIC_DETERMINISTIC) return false;
+  // the gathering push swaps the species' buffers on the host: not replayable
+  for (const auto& s : c.species)
+    if (s.perm_pending) return false;
   if (c.phase_timing || !c.emitters.empty() || c.laser.e0 != 0.f) return false;
   if (absorbing_walls(c)) return false;
   return c.use_graphs;
@@ -830,7 +838,12 @@ int pic_internal_set_graphs(pic_context* ctx, int on) {
 int pic_step_host(pic_context* ctx, unsigned flags, float* const* lanes7, int32_t* const* ids) {
   return guard([&] {
     Context& c = C_(ctx);
-    if (c.gc.xopen) throw UsageError("pic_step_host: x-open (decomposed) or walled context");
+    // host arrays keep their length: no exchange, absorption or emission
+    if (c.gc.xopen || has_walls(c) || !c.emitters.empty())
+      throw UsageError("pic_step_host: x-open (decomposed), walled or emitting context (use pic_step)");
+    if (!lanes7 || !ids) throw UsageError("pic_step_host: null buffer list");
+    for (size_t s = 0; s < c.species.size(); ++s)
+      if (c.species[s].n && (!lanes7[s] || !ids[s])) throw UsageError("pic_step_host: null species buffer");
     if (flags & PIC_DETERMINISTIC) {
       // ordered replay needs whole-species passes: upload, step, download
       for (size_t s = 0; s < c.species.size(); ++s) {
@@ -1096,7 +1109,7 @@ int pic_internal_set_sort_variant(pic_context* ctx, int variant) {
 }
 // Not in the public header: selects an advance_p strategy (benchmarking).
 int pic_internal_set_push_variant(pic_context* ctx, int variant) {
-  return guard([&] { C_(ctx).push_variant = variant; });
+  return guard([&] { set_push_variant(C_(ctx), variant); });
 }
 
 // Not in the public header: particles per chunk of the pic_step_host pipeline.

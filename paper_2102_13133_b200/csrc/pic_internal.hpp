@@ -239,10 +239,33 @@ void materialize_all(Context& c);
 // 8-bit digits; 3 = radix, 9-bit, per-bit ballot grouping; 4 = 8-bit, ballot.
 // Measured on B200, 2^29 particles 19 steps after a sort: 17.6 / 28 / 17.9 /
 // 23.0 / 20.6 ms.
+inline bool ablations_built() {
+#ifdef PIC_ABLATIONS
+  return true;
+#else
+  return false;
+#endif
+}
 inline void set_sort_variant(Context& c, int v) {
+  if (v != 0 && !(ablations_built() && v >= 0 && v <= 4))
+    throw UsageError("sort variant " + std::to_string(v) +
+                     " is not in this build (ablations: libpic_b200_ablate.so)");
   c.sort_variant = v == 1 ? 1 : 0;
   c.sort_radix_bits = (v == 2 || v == 4) ? 8 : 9;
   c.sort_match = (v == 3 || v == 4) ? 0 : 1;
+}
+
+// advance_p strategy: the product library holds 52 (advance_p_lean, the
+// default) and 42 (advance_p_run: exact_gyration, decks outside the
+// call-free ranges); the measured ablations (0-55) and the timing probes
+// (90-93, 99: not valid pushes) exist only in libpic_b200_ablate.so.
+inline void set_push_variant(Context& c, int v) {
+  const bool product = v == 42 || v == 52;
+  const bool ablation = (v >= 0 && v <= 55) || (v >= 90 && v <= 93) || v == 99;
+  if (!product && !(ablations_built() && ablation))
+    throw UsageError("push variant " + std::to_string(v) +
+                     " is not in this build (ablations: libpic_b200_ablate.so)");
+  c.push_variant = v;
 }
 
 // ---- the step --------------------------------------------------------------

@@ -613,6 +613,13 @@ static size_t copy_out(const std::string& s, char* buf, size_t cap) {
   return s.size();
 }
 
+// the sim's device is current for every call (several GPUs, one host thread)
+static Sim& S_(pic_sim* s) {
+  if (!s || !s->s) throw UsageError("null pic_sim");
+  CUDA_OK(cudaSetDevice(s->s->ctx->device));
+  return *s->s;
+}
+
 extern "C" {
 
 int pic_deck_parse(const char* text, pic_deck** out) {
@@ -678,38 +685,38 @@ int pic_sim_context(pic_sim* s, pic_context** out) {
 }
 int pic_sim_step(pic_sim* s) {
   return capi_guard([&] {
-    if (!s) throw UsageError("pic_sim_step: null sim");
-    s->s->do_step();
-    s->s->sort_due();
-    quiesce(*s->s->ctx);
+    Sim& m = S_(s);
+    m.do_step();
+    m.sort_due();
+    quiesce(*m.ctx);
   });
 }
 int pic_sim_step_count(pic_sim* s, long* out) {
-  return capi_guard([&] { *out = s->s->step_count; });
+  return capi_guard([&] { *out = S_(s).step_count; });
 }
 int pic_sim_refresh_charge_diagnostics(pic_sim* s) {
-  return capi_guard([&] { s->s->refresh_charge(); });
+  return capi_guard([&] { S_(s).refresh_charge(); });
 }
 int pic_sim_emit_diagnostics(pic_sim* s, char* buf, size_t cap, size_t* len) {
   return capi_guard([&] {
-    const size_t n = copy_out(s->s->diagnostics_row(), buf, cap);
+    const size_t n = copy_out(S_(s).diagnostics_row(), buf, cap);
     if (len) *len = n;
   });
 }
 int pic_sim_run(pic_sim* s, const char* csv_path) {
   return capi_guard([&] {
-    if (!s) throw UsageError("pic_sim_run: null sim");
+    Sim& m = S_(s);
     if (csv_path) {
       std::ofstream f(csv_path);
       if (!f) throw RunAbort(std::string("pic_sim_run: cannot open ") + csv_path);
-      s->s->run(&f);
+      m.run(&f);
     } else {
-      s->s->run(nullptr);
+      m.run(nullptr);
     }
   });
 }
 int pic_sim_dump_fields(pic_sim* s, const char* path) {
-  return capi_guard([&] { s->s->dump_fields(path); });
+  return capi_guard([&] { S_(s).dump_fields(path); });
 }
 int pic_sim_warnings(pic_sim* s, char* buf, size_t cap, size_t* len) {
   return capi_guard([&] {

@@ -361,6 +361,7 @@ __global__ void permute_kernel(const unsigned* __restrict__ perm, size_t n, cons
 
 inline unsigned blocks_for(size_t n, int t = 256) { return (unsigned)((n + t - 1) / t); }
 
+#ifdef PIC_ABLATIONS
 // ---- tiled stable counting sort (blocked order) ---------------------------------
 // The stable counting sort of sort_particles (particles.cpp:419-433) split in
 // tiles of kCT consecutive particles: (A) each tile sorts its keys stably in
@@ -495,7 +496,9 @@ tile_scatter_kernel(const unsigned* __restrict__ meta, size_t n, const unsigned*
   }
 }
 
+#endif  // PIC_ABLATIONS
 }  // namespace
+#ifdef PIC_ABLATIONS
 
 // Stable blocked sort of species s by voxel id into (pos_alt, mom_alt).
 static void tiled_counting_sort(Context& c, Species& s) {
@@ -536,6 +539,8 @@ static void tiled_counting_sort(Context& c, Species& s) {
   c.count_launch(8);
 }
 
+
+#endif  // PIC_ABLATIONS
 
 int key_bits_for(long long max_key_exclusive) {
   int b = 1;
@@ -682,12 +687,14 @@ void sort_species(Context& c, Species& s, int order) {
     CUDA_OK(cudaMalloc(&s.pos_alt, s.cap * sizeof(float4)));
     CUDA_OK(cudaMalloc(&s.mom_alt, s.cap * sizeof(float4)));
   }
+#ifdef PIC_ABLATIONS
   if (order == PIC_SORT_BLOCKED && c.sort_variant == 1) {
     tiled_counting_sort(c, s);
     std::swap(s.pos, s.pos_alt);
     std::swap(s.mom, s.mom_alt);
     return;
   }
+#endif
   const int kbits = key_bits_for(c.gc.V);
   // keys out of the records, fused with the first pass's tile histogram
   unsigned* keys = static_cast<unsigned*>(c.scratch_bytes(Context::kScrCount, n * 4));

@@ -28,10 +28,35 @@ def test_reference_arm_runs_the_compiled_reference():
     if not ref_available():
         import pytest
         pytest.skip("oracle/_ref not built")
-    d = _run("--impl", "reference", "--steps", "1", "--warmup", "1", "--cpu-sample-n", "12")
+    d = _run("--impl", "reference", "--steps", "3", "--warmup", "2", "--cpu-sample-n", "12")
     assert d["impl"] == "reference" and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "reference" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0
+    # the line reports the steps it timed and names its bounded sample
+    assert d["steps"] == 3 and d["warmup"] == 2
+    assert d["config"]["sample_cells"] == "12^3" and d["config"]["same_config"] is False
+    assert d["config"]["workload"] == "two_stream" and d["config"]["cells"] == "256^3"
+    assert d["metric"].startswith("particle pushes/sec summed over all GPUs")
+
+
+def test_reference_arm_sort_cadence_inside_window():
+    """With a sort point among the timed steps the reference's own run-loop
+    sort is timed (nothing amortised separately)."""
+    from oracle.bindings import ref_available
+    if not ref_available():
+        import pytest
+        pytest.skip("oracle/_ref not built")
+    d = _run("--impl", "reference", "--steps", "20", "--warmup", "1", "--cpu-sample-n", "8")
+    assert d["steps"] == 20 and "amortised" not in d["config"]["sample"]
+
+
+def test_aggregate_value_and_per_gpu(monkeypatch):
+    """value is the whole-job sum over ranks and value_per_gpu = value / N
+    (BASELINE.json's per-GPU metric), for the kernel line and e2e alike."""
+    src = open(os.path.join(ROOT, "bench.py")).read()
+    assert '"value_per_gpu": value / world' in src
+    assert 'npart_all * k / dt / world' in src
+    assert 'float(tn.item()) * k / dt / world' in src
 
 
 def test_configs():
