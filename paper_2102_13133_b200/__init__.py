@@ -534,6 +534,39 @@ class Context:
         fn.argtypes = [C.c_void_p, C.c_int]
         check(fn(self._h, variant))
 
+    def _set_voxel_order(self, on: bool):
+        """A/B hook (not in the public C header): continuous voxel order of the
+        fast push (default on); off returns every species to logical order."""
+        fn = lib().pic_internal_set_voxel_order
+        fn.argtypes = [C.c_void_p, C.c_int]
+        check(fn(self._h, int(on)))
+
+    def _set_reorder_interval(self, m: int):
+        """Tuning hook (not in the public C header): every m-th ordered push
+        reorders the store."""
+        fn = lib().pic_internal_set_reorder_interval
+        fn.argtypes = [C.c_void_p, C.c_int]
+        check(fn(self._h, m))
+
+    def _species_ordered(self, sid: int) -> bool:
+        """Test hook: whether the species is held in continuous voxel order."""
+        fn = lib().pic_internal_species_ordered
+        out = C.c_int()
+        check(fn(self._h, sid, C.byref(out)))
+        return bool(out.value)
+
+    def _download_physical(self, sid: int):
+        """Test hook: (pos, mom) float32 (n, 4) records as they lie in memory
+        and, in continuous voxel order, their logical indices."""
+        n = self.species_count(sid)
+        pos = np.zeros((n, 4), np.float32)
+        mom = np.zeros((n, 4), np.float32)
+        lidx = np.zeros(n, np.uint32)
+        fn = lib().pic_internal_download_physical
+        fn.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
+        check(fn(self._h, sid, pos.ctypes.data, mom.ctypes.data, lidx.ctypes.data))
+        return pos, mom, lidx
+
     def _set_graphs(self, on: bool):
         """Benchmarking hook (not in the public C header): pic_step as CUDA graphs."""
         fn = lib().pic_internal_set_graphs

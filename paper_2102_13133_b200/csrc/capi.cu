@@ -82,6 +82,11 @@ void Context::release() {
     cudaFree(s.pos_alt);
     cudaFree(s.mom_alt);
     cudaFree(s.perm);
+    cudaFree(s.lidx);
+    cudaFree(s.lidx_alt);
+    cudaFree(s.vcur);
+    cudaFree(s.vcnt);
+    cudaFree(s.vscan);
     cudaFree(s.mig_idx);
     cudaFree(s.mig_count);
   }
@@ -169,6 +174,8 @@ Context* make_context(int device, const pic_grid& g) {
     if (const char* v = std::getenv("PIC_FORK_SPECIES")) c->fork_species = std::atoi(v) != 0;  // profiling knob
     if (const char* v = std::getenv("PIC_SORT_VARIANT")) set_sort_variant(*c, std::atoi(v));  // profiling knob
     if (const char* v = std::getenv("PIC_SORT_DEFER")) c->sort_defer = std::atoi(v) != 0;     // profiling knob
+    if (const char* v = std::getenv("PIC_VOXEL_ORDER")) c->voxel_order = std::atoi(v) != 0;   // profiling knob
+    if (const char* v = std::getenv("PIC_REORDER_INTERVAL")) c->reorder_interval = std::atoi(v);  // profiling knob
     if (const char* v = std::getenv("PIC_HOST_BUFS")) c->host_bufs = std::atoi(v);            // profiling knob
     const size_t V = (size_t)gc.V;
     CUDA_OK(cudaMalloc(&c->f, F_COUNT * V * sizeof(float)));
@@ -329,7 +336,12 @@ void step(Context& c, unsigned flags) {
 // pinned (pic_host_register) for the copies to overlap.
 static void step_host(Context& c, unsigned flags, float* const* lanes7, int32_t* const* ids) {
   const bool exact = (flags & PIC_EXACT_GYRATION) != 0;
-  for (auto& s : c.species) s.perm_pending = false;  // the host arrays replace the device records
+  for (auto& s : c.species) {  // the host arrays replace the device records
+    s.perm_pending = false;
+    s.ordered = false;
+    s.relabel_pending = false;
+    s.counts_ready = false;
+  }
   size_t nmax = 0;
   for (auto& s : c.species) nmax = std::max(nmax, s.n);
   const size_t chunk = std::max<size_t>(1, std::min<size_t>(nmax, c.host_chunk));
@@ -381,7 +393,7 @@ static void step_host(Context& c, unsigned flags, float* const* lanes7, int32_t*
       CUDA_OK(cudaStreamWaitEvent(c.stream, c.ev_in[b], 0));
       launch_pack_species(c, view, reinterpret_cast<float*>(in), reinterpret_cast<int32_t*>(in + cnt * 28), cnt);
       CUDA_OK(cudaEventRecord(c.ev_packed[b], c.stream));
-      launch_advance_p(c, view, exact);
+      launch_advance_p(c, view, exact, false);
       CUDA_OK(cudaStreamWaitEvent(c.stream, c.ev_out[b], 0));
       launch_unpack_species(c, view, reinterpret_cast<float*>(out), reinterpret_cast<int32_t*>(out + cnt * 28));
       CUDA_OK(cudaEventRecord(c.ev_unpacked[b], c.stream));
@@ -739,7 +751,7 @@ int pic_sort_particles(pic_context* ctx, int species, int order) {
     if (order != PIC_SORT_BLOCKED && order != PIC_SORT_INTERLEAVED) throw UsageError("sort: bad order");
     Context& c = C_(ctx);
     c.phase_begin(Context::kPhSort);
-    sort_species(c, species_at(c, species), order);
+    sort_species(c, species_ref(c, species), order);  // resolves any pending order itself
     c.phase_end();
     check_launch();
   });
@@ -753,9 +765,6 @@ int pic_sort_particles(pic_context* ctx, int species, int order) {
 // the laser (host-computed amplitude), phase timing (host events).
 static bool graph_ok(const Context& c, unsigned flags) {
   if (flags & PIC_DETERMINISTIC) return false;
-  // the gathering push swaps the species' buffers on the host: not replayable
-  for (const auto& s : c.species)
-    if (s.perm_pending) return false;
   if (c.phase_timing || !c.emitters.empty() || c.laser.e0 != 0.f) return false;
   if (absorbing_walls(c)) return false;
   return c.use_graphs;
@@ -767,10 +776,38 @@ static std::vector<uint64_t> graph_key(const Context& c, unsigned flags) {
   for (const auto& s : c.species) {
     k.push_back((uint64_t)(uintptr_t)s.pos);
     k.push_back((uint64_t)(uintptr_t)s.mom);
+    k.push_back((uint64_t)(uintptr_t)s.lidx);
     k.push_back((uint64_t)s.n);
-    k.push_back(s.perm_pending ? 1u : 0u);
+    k.push_back((s.perm_pending ? 1u : 0u) | (s.ordered ? 2u : 0u) | (s.relabel_pending ? 4u : 0u) |
+                (s.counts_ready ? 8u : 0u) | ((uint64_t)s.since_reorder << 8));
   }
   return k;
+}
+
+static std::vector<Context::SpeciesState> species_state(const Context& c) {
+  std::vector<Context::SpeciesState> v;
+  for (const auto& s : c.species)
+    v.push_back({s.pos, s.mom, s.pos_alt, s.mom_alt, s.lidx, s.lidx_alt, s.perm_pending, s.ordered,
+                 s.relabel_pending, s.counts_ready, s.since_reorder});
+  return v;
+}
+
+static void apply_species_state(Context& c, const std::vector<Context::SpeciesState>& v) {
+  for (size_t i = 0; i < v.size() && i < c.species.size(); ++i) {
+    Species& s = c.species[i];
+    const auto& t = v[i];
+    s.pos = t.pos;
+    s.mom = t.mom;
+    s.pos_alt = t.pos_alt;
+    s.mom_alt = t.mom_alt;
+    s.lidx = t.lidx;
+    s.lidx_alt = t.lidx_alt;
+    s.perm_pending = t.perm_pending;
+    s.ordered = t.ordered;
+    s.relabel_pending = t.relabel_pending;
+    s.counts_ready = t.counts_ready;
+    s.since_reorder = t.since_reorder;
+  }
 }
 
 void step_graphed(Context& c, unsigned flags) {
@@ -782,13 +819,16 @@ void step_graphed(Context& c, unsigned flags) {
   for (auto& g : c.graphs) {
     if (g.key == key) {
       CUDA_OK(cudaGraphLaunch(g.exec, c.stream));
+      apply_species_state(c, g.post);
       c.count_launch(g.launches);
       ++c.steps_done;
       return;
     }
   }
-  if (c.graph_seen != key) {  // first step of a configuration: plain (allocates scratch, sets attributes)
-    c.graph_seen = key;
+  if (std::find(c.graph_seen.begin(), c.graph_seen.end(), key) == c.graph_seen.end()) {
+    // first step of a configuration: plain (allocates scratch, sets attributes)
+    c.graph_seen.push_back(key);
+    if (c.graph_seen.size() > 32) c.graph_seen.erase(c.graph_seen.begin());
     step(c, flags);
     return;
   }
@@ -807,11 +847,12 @@ void step_graphed(Context& c, unsigned flags) {
   Context::Graph g;
   g.key = key;
   g.launches = c.launches - l0;
+  g.post = species_state(c);
   CUDA_OK(cudaGraphInstantiate(&g.exec, graph, 0));
   CUDA_OK(cudaGraphDestroy(graph));
   c.launches = l0;
   c.steps_done = sd;
-  if (c.graphs.size() >= 4) {
+  if (c.graphs.size() >= 24) {
     CUDA_OK(cudaGraphExecDestroy(c.graphs.front().exec));
     c.graphs.erase(c.graphs.begin());
   }
@@ -1007,7 +1048,7 @@ int pic_compute_div_errors(pic_context* ctx) {
 int pic_refresh_charge_diagnostics(pic_context* ctx) {
   return guard([&] {
     Context& c = C_(ctx);
-    materialize_all(c);
+    materialize_for_sums(c);
     launch_clear_rho(c);
     for (auto& s : c.species) launch_deposit_rho(c, s);
     launch_compute_div_errors(c);
@@ -1032,7 +1073,8 @@ int pic_max_abs_lane(pic_context* ctx, int lane, float* out) {
 int pic_kinetic_energy(pic_context* ctx, int species, int centered, float* out) {
   return guard([&] {
     Context& c = C_(ctx);
-    Species& s = species_at(c, species);
+    Species& s = species_ref(c, species);
+    if (!s.ordered) materialize(c, s);  // order-free sum
     quiesce(c);
     *out = kinetic_energy(c, s, centered != 0);
   });
@@ -1041,7 +1083,7 @@ int pic_diagnostics(pic_context* ctx, pic_diag* out, float* kinetic, size_t kine
   return guard([&] {
     Context& c = C_(ctx);
     if (!out) throw UsageError("diagnostics: null output");
-    materialize_all(c);
+    materialize_for_sums(c);
     if (kinetic_cap < c.species.size() || (!kinetic && !c.species.empty()))
       throw UsageError("diagnostics: kinetic[] smaller than the species count");
     quiesce(c);
@@ -1110,6 +1152,44 @@ int pic_internal_set_sort_variant(pic_context* ctx, int variant) {
 // Not in the public header: selects an advance_p strategy (benchmarking).
 int pic_internal_set_push_variant(pic_context* ctx, int variant) {
   return guard([&] { set_push_variant(C_(ctx), variant); });
+}
+
+// Not in the public header: continuous voxel order of the fast push on / off
+// (benchmarking and A/B tests); off leaves every species in logical order.
+int pic_internal_set_voxel_order(pic_context* ctx, int on) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    c.voxel_order = on != 0;
+    if (!c.voxel_order)
+      for (auto& s : c.species) leave_voxel_order(c, s);
+  });
+}
+// Not in the public header: pushes between reorderings of the store.
+int pic_internal_set_reorder_interval(pic_context* ctx, int m) {
+  return guard([&] {
+    if (m < 1) throw UsageError("reorder interval must be >= 1");
+    C_(ctx).reorder_interval = m;
+  });
+}
+// Not in the public header: 1 when the species is held in continuous voxel order.
+int pic_internal_species_ordered(pic_context* ctx, int species, int* out) {
+  return guard([&] { *out = species_ref(C_(ctx), species).ordered ? 1 : 0; });
+}
+
+// Not in the public header: the species' records as they lie (no order
+// applied) plus, in continuous voxel order, the logical index of each
+// (diagnostics of the physical layout).
+int pic_internal_download_physical(pic_context* ctx, int species, void* pos16, void* mom16, unsigned* lidx) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    Species& s = species_ref(c, species);
+    quiesce(c);
+    if (s.n == 0) return;
+    CUDA_OK(cudaMemcpyAsync(pos16, s.pos, s.n * 16, cudaMemcpyDefault, c.stream));
+    CUDA_OK(cudaMemcpyAsync(mom16, s.mom, s.n * 16, cudaMemcpyDefault, c.stream));
+    if (lidx && s.ordered) CUDA_OK(cudaMemcpyAsync(lidx, s.lidx, s.n * 4, cudaMemcpyDefault, c.stream));
+    CUDA_OK(cudaStreamSynchronize(c.stream));
+  });
 }
 
 // Not in the public header: particles per chunk of the pic_step_host pipeline.

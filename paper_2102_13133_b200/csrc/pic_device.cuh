@@ -91,6 +91,21 @@ __device__ __forceinline__ void st_stream(float4* p, float4 v) {
                "f"(v.y), "f"(v.z), "f"(v.w)
                : "memory");
 }
+// Stores / loads that do not allocate in L1 (the ordered push's scattered
+// output must not evict the interpolator records the gathers reuse).
+__device__ __forceinline__ void st_na(float4* p, float4 v) {
+  asm volatile("st.global.L1::no_allocate.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void st_na_u32(unsigned* p, unsigned v) {
+  asm volatile("st.global.L1::no_allocate.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_na_u32(const unsigned* p) {
+  unsigned r;
+  asm volatile("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
 __device__ __forceinline__ void red_add_v4(float* addr, float a, float b, float c,
                                            float d) {
   asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(addr), "f"(a),

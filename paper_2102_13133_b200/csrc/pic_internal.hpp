@@ -59,6 +59,19 @@ struct Species {
   // other consumer materialises it first (materialize()).
   unsigned* perm = nullptr;  // cap entries (lazy)
   bool perm_pending = false;
+  // Voxel order of the fast push's store (order.cu): physical record i is
+  // logical (reference-order) record lidx[i]; vcnt = records per voxel,
+  // vcur = chunk cursors of the reordering push (lazy; V entries), vscan =
+  // the count scan's tile sums.
+  unsigned* lidx = nullptr;
+  unsigned* lidx_alt = nullptr;
+  unsigned* vcur = nullptr;
+  unsigned* vcnt = nullptr;
+  unsigned* vscan = nullptr;  // tile sums of the count scan
+  bool ordered = false;          // physical order != logical; lidx valid
+  bool relabel_pending = false;  // a blocked sort is owed (applied by the next push, a reordering one)
+  bool counts_ready = false;     // vcur = chunk starts of the stored voxels (the last push counted)
+  unsigned since_reorder = 0;    // pushes since the last reordering one
 };
 
 struct Context {
@@ -87,6 +100,8 @@ struct Context {
   int sort_radix_bits = 9;  // LSD digit width (passes = ceil(key bits / width), widths evened out)
   int sort_match = 1;       // group equal digits with match.any (0: per-bit ballots)
   bool sort_defer = true;   // blocked sorts leave the permutation to the next push
+  bool voxel_order = true;  // fast periodic pushes keep the store near voxel order (order.cu)
+  int reorder_interval = 5;  // every m-th ordered push reorders the store (PIC_REORDER_INTERVAL)
   int num_sms = 148;
   // non-periodic x boundaries (boundary.cu): absorbed particle counts per
   // side, the laser source, emitter hooks, steps taken (laser clock)
@@ -101,13 +116,23 @@ struct Context {
   long long steps_done = 0;
   bool decomposed = false;  // pic_set_x_open: x faces exchanged by the host
   // pic_step as CUDA graphs (capi.cu step_graphed): a few configurations
+  // The species' host-side state a step leaves behind (buffer swaps of the
+  // ordered push / gathering push, order flags): a graph replay re-applies
+  // the state its capture produced.
+  struct SpeciesState {
+    float4 *pos, *mom, *pos_alt, *mom_alt;
+    unsigned *lidx, *lidx_alt;
+    bool perm_pending, ordered, relabel_pending, counts_ready;
+    unsigned since_reorder;
+  };
   struct Graph {
     std::vector<uint64_t> key;
     cudaGraphExec_t exec = nullptr;
     uint64_t launches = 0;
+    std::vector<SpeciesState> post;
   };
   std::vector<Graph> graphs;
-  std::vector<uint64_t> graph_seen;
+  std::vector<std::vector<uint64_t>> graph_seen;  // recent keys (captured on their second occurrence)
   bool use_graphs = true;
   cudaEvent_t events[64] = {};
   // fast-mode step: species after the first push on side streams (their
@@ -163,7 +188,9 @@ void quiesce(Context& c);
 Species& species_at(Context& c, int sid);
 
 // ---- launchers -------------------------------------------------------------
-void launch_advance_p(Context& c, Species& s, bool exact_gyration);
+// ordered: the fast push may keep the store in continuous voxel order (not
+// for chunk views of a species, pic_step_host)
+void launch_advance_p(Context& c, Species& s, bool exact_gyration, bool ordered = true);
 void launch_advance_p_deterministic(Context& c, Species& s, bool exact_gyration);
 void launch_load_interpolators(Context& c);
 // images: also write B's periodic ghost images (the step's fused ghost sync)
@@ -231,9 +258,16 @@ void key_run_starts(Context& c, const unsigned* skey, size_t n, size_t V, unsign
 void radix_sort_pairs(Context& c, const unsigned* keys, const unsigned* vals, size_t n,
                       int key_bits, unsigned** keys_out, unsigned** vals_out);
 void sort_species(Context& c, Species& s, int order);
+// continuous voxel order (order.cu)
+bool voxel_order_usable(const Context& c);
+void enter_voxel_order(Context& c, Species& s);  // logical indices of the current store
+void prepare_reorder(Context& c, Species& s);    // chunk cursors of the stored voxels
+void after_ordered_push(Context& c, Species& s, bool reordered, bool counted);
+void leave_voxel_order(Context& c, Species& s);   // records back into logical order
 // apply a deferred sort permutation (no-op when none is pending)
 void materialize(Context& c, Species& s);
 void materialize_all(Context& c);
+void materialize_for_sums(Context& c);
 // Sort strategies (benchmarking): 0 = LSD radix, 9-bit digits, equal digits
 // grouped with match.any (default); 1 = tiled counting sort; 2 = radix,
 // 8-bit digits; 3 = radix, 9-bit, per-bit ballot grouping; 4 = 8-bit, ballot.

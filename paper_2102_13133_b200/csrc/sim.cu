@@ -496,7 +496,7 @@ struct Sim {
 
   void refresh_charge() {  // SimState::refresh_charge_diagnostics (sim.cpp:230-234)
     launch_clear_rho(*ctx);
-    materialize_all(*ctx);
+    materialize_for_sums(*ctx);
     for (auto& s : ctx->species) launch_deposit_rho(*ctx, s);
     launch_compute_div_errors(*ctx);
   }

@@ -665,6 +665,7 @@ void radix_sort_pairs(Context& c, const unsigned* keys, const unsigned* vals, si
 }
 
 void materialize(Context& c, Species& s) {
+  leave_voxel_order(c, s);  // continuous voxel order -> logical order (+ an owed sort)
   if (!s.perm_pending) return;
   s.perm_pending = false;
   if (s.n == 0) return;
@@ -677,9 +678,23 @@ void materialize(Context& c, Species& s) {
 void materialize_all(Context& c) {
   for (auto& s : c.species) materialize(c, s);
 }
+// Order-free reads (charge deposit, energy sums): a species in continuous
+// voxel order is read where it lies (its n records are all valid); only a
+// deferred sort permutation is applied.
+void materialize_for_sums(Context& c) {
+  for (auto& s : c.species)
+    if (!s.ordered) materialize(c, s);
+}
 
 // sort_particles (particles.cpp:412-458).
 void sort_species(Context& c, Species& s, int order) {
+  if (s.ordered && order == PIC_SORT_BLOCKED) {
+    // owed to the next push, a reordering one: it groups the store by
+    // exactly these voxels, so the stable counting sort becomes a
+    // relabelling of the logical indices (order.cu)
+    s.relabel_pending = true;
+    return;
+  }
   materialize(c, s);
   const size_t n = s.n;
   if (n == 0) return;

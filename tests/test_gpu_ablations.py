@@ -35,7 +35,7 @@ wacc = np.zeros((g.padded, 12), np.float32)
 orc.advance_particles(o, -1.0, 1.0, wp, wids, interp, wacc, False)
 for v in list(range(56)):
     with pic.Context(g) as ctx:
-        sid = ctx.add_species("s", -1.0, 1.0, p.shape[0])
+        sid = ctx.add_species("s", -1.0, 1.0, ids.size)
         ctx._set_push_variant(v)
         ctx.upload_species(sid, p, ids)
         ctx.upload_fields(f)
@@ -55,7 +55,7 @@ for order in (0, 1):
     for v in range(5):
         with pic.Context(g) as ctx:
             ctx._set_sort_variant(v)
-            sid = ctx.add_species("s", -1.0, 1.0, ps.shape[0])
+            sid = ctx.add_species("s", -1.0, 1.0, idss.size)
             ctx.upload_species(sid, ps, idss)
             ctx.sort_particles(sid, order)
             gp, gids = ctx.download_species(sid)
