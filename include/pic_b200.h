@@ -316,6 +316,15 @@ typedef struct pic_diag {
  * errors, particle count.  Call pic_refresh_charge_diagnostics first for
  * current div errors, as SimState::run does on the diag cadence. */
 int pic_diagnostics(pic_context* ctx, pic_diag* out, float* kinetic, size_t kinetic_cap);
+/* Energy summation order of pic_diagnostics / pic_field_energy /
+ * pic_kinetic_energy (centered): 0 (default) = fp64 device sums of the
+ * reference's fp32 terms; 1 = the reference's own fp32 order (sum_squares'
+ * 8 interleaved partials per x line, lines summed serially in (lane, z, y)
+ * order, fields.cpp:276-299, kernels/scalar.cpp:51-59; kinetic: 8 interleaved
+ * partials over the particles in order, particles.cpp:468-501) —
+ * bit-identical to the reference in deterministic mode, serial chains of
+ * n/8 adds.  pic_sim sets 1 for decks with run.deterministic = true. */
+int pic_diagnostics_order(pic_context* ctx, int reference_order);
 
 /* ---- decks and the SimState run surface ---------------
  * The reference's host API above the step: the deck text format
@@ -327,7 +336,7 @@ int pic_diagnostics(pic_context* ctx, pic_diag* out, float* kinetic, size_t kine
  * state is bit-identical to SimState::initialize's.  Deck keys that pick CPU
  * strategies (run.workers, layout, scatter_backend, chunk_size, kernel) are
  * validated and ignored; run.deterministic / exact_gyration map to the
- * PIC_* flags.  Hooks are not part of the C surface. */
+ * PIC_* flags. */
 typedef struct pic_deck pic_deck;
 typedef struct pic_sim pic_sim;
 /* parse_deck (deck.cpp:200-293): PIC_DECK_PARSE_ERROR names key and line. */
@@ -360,6 +369,37 @@ int pic_sim_run(pic_sim* sim, const char* csv_path);
 int pic_sim_dump_fields(pic_sim* sim, const char* path);
 /* SimState::warnings (sim.hpp:171), newline-separated. */
 int pic_sim_warnings(pic_sim* sim, char* buf, size_t cap, size_t* len);
+
+/* Hooks (HookRegistration / HookFlags / HookContext, proj/include/minipic/
+ * sim.hpp:102-127; SimState::run_hooks, proj/src/sim.cpp:185-215): run by
+ * pic_sim_run after the step, the due sorts and the due charge refresh,
+ * every `interval` steps (never at step 0).  The flags say which host
+ * mirrors are refreshed from the device before the callback
+ * (particles_to_host: every species' 7 lanes + ids in the reference's order;
+ * fields_to_host: the 16 field lanes) and copied back after it
+ * (particles_back, fields_back; particle counts are fixed).  Every mirror
+ * copy is one copy in pic_sim_copies_performed (copy_between's count,
+ * proj/src/layout.cpp:99-118): the legacy flags (all four; flags == NULL)
+ * cost 2 x species + 2 copies per invocation, none cost nothing.  A callback
+ * returning nonzero aborts the run: PIC_RUN_ABORT "hook '<name>' failed at
+ * step <n>: ...". */
+typedef struct pic_hook_flags {
+  int particles_to_host, fields_to_host, particles_back, fields_back;
+} pic_hook_flags;
+typedef struct pic_hook_view {
+  pic_sim* sim;
+  long step;
+  float* fields16;        /* 16 x V, lane-major (the reference's field-major layout) */
+  size_t nspecies;
+  float* const* lanes7;   /* per species: 7 x n, lane-major */
+  int32_t* const* ids;    /* per species: n voxel ids */
+  const size_t* counts;   /* per species: n */
+} pic_hook_view;
+typedef int (*pic_hook_fn)(pic_hook_view* view, void* user);
+int pic_sim_register_hook(pic_sim* sim, const char* name, long interval, const pic_hook_flags* flags,
+                          pic_hook_fn fn, void* user);
+/* SimState::copies_performed (sim.hpp:175): mirror copies since initialize. */
+int pic_sim_copies_performed(pic_sim* sim, uint64_t* out);
 
 /* ---- timing: CUDA events on the context stream --------------------------*/
 int pic_event_record(pic_context* ctx, int slot); /* slot in [0, 64) */

@@ -245,6 +245,7 @@ class Ref:
         L.mref_sim_step_count.restype = C.c_long
         L.mref_sim_run_csv.argtypes = [C.c_void_p, C.c_char_p, C.c_long]
         L.mref_sim_timings.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
+        L.mref_sim_diagnostics.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_double), C.c_int]
 
     def _chk(self, rc):
         if rc:
@@ -380,6 +381,15 @@ class RefSim:
     @property
     def step_count(self):
         return self.ref.lib.mref_sim_step_count(self.h)
+
+    def diagnostics(self, refresh=False) -> dict:
+        """SimState::current_diagnostics (after refresh_charge_diagnostics if
+        asked), as floats."""
+        out = np.zeros(6 + self.nspecies, np.float64)
+        self.ref._chk(self.ref.lib.mref_sim_diagnostics(self.h, int(refresh), out.ctypes.data_as(C.POINTER(C.c_double)),
+                                                        out.size))
+        return {"e_energy": out[0], "b_energy": out[1], "total_energy": out[2], "max_div_e_err": out[3],
+                "max_div_b_err": out[4], "particle_count": int(out[5]), "kinetic": list(out[6:])}
 
     def run_csv(self, cap=1 << 22) -> str:
         buf = C.create_string_buffer(cap)

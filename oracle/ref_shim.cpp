@@ -361,6 +361,24 @@ int mref_sim_step_and_sort(void* h, long nsteps) {
   });
 }
 long mref_sim_step_count(void* h) { return static_cast<SimHandle*>(h)->s->step_count(); }
+// SimState::refresh_charge_diagnostics (optional) + current_diagnostics
+// (proj/src/sim.cpp:230-266): out = e_energy, b_energy, total_energy,
+// max_div_e_err, max_div_b_err, particle_count, kinetic[0..k)
+int mref_sim_diagnostics(void* h, int refresh, double* out, int cap) {
+  return guard([&] {
+    SimState& s = *static_cast<SimHandle*>(h)->s;
+    if (refresh) s.refresh_charge_diagnostics();
+    const DiagnosticsRecord d = s.current_diagnostics();
+    if (cap < 6 + static_cast<int>(d.kinetic.size())) throw usage_error("diagnostics buffer too small");
+    out[0] = d.e_energy;
+    out[1] = d.b_energy;
+    out[2] = d.total_energy;
+    out[3] = d.max_div_e_err;
+    out[4] = d.max_div_b_err;
+    out[5] = static_cast<double>(d.particle_count);
+    for (std::size_t k = 0; k < d.kinetic.size(); ++k) out[6 + k] = d.kinetic[k];
+  });
+}
 int mref_sim_run_csv(void* h, char* buf, long buflen) {
   return guard([&] {
     std::ostringstream os;

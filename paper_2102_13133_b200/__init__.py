@@ -180,6 +180,7 @@ def lib() -> C.CDLL:
         "pic_max_abs_lane": [P, C.c_int, C.POINTER(C.c_float)],
         "pic_kinetic_energy": [P, C.c_int, C.c_int, C.POINTER(C.c_float)],
         "pic_diagnostics": [P, C.POINTER(Diag), C.POINTER(C.c_float), C.c_size_t],
+        "pic_diagnostics_order": [P, C.c_int],
         "pic_set_x_open": [P, C.c_int, C.c_int],
         "pic_set_stream": [P, P],
         "pic_halo_plane_bytes": [P, C.c_int, C.POINTER(C.c_size_t)],
@@ -498,6 +499,11 @@ class Context:
         out = C.c_float()
         check(lib().pic_kinetic_energy(self._h, sid, int(centered), C.byref(out)))
         return out.value
+
+    def diagnostics_order(self, reference_order: bool):
+        """Energies summed in the reference's fp32 order (bit-identical in
+        deterministic mode) or as fp64 device sums (default)."""
+        check(lib().pic_diagnostics_order(self._h, int(reference_order)))
 
     def diagnostics(self) -> dict:
         """SimState::current_diagnostics (sim.cpp:236-266) on the device."""

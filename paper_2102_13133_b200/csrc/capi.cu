@@ -13,12 +13,17 @@
 #include <exception>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "pic_internal.hpp"
 
 namespace picb {
 
 namespace {
 thread_local std::string g_last_error;
+// NVTX range names of the PhaseTimings phases (header-only NVTX3: no cost
+// unless a tool is attached)
+const char* const kPhaseName[Context::kPhN] = {"interpolate", "push", "scatter", "field", "sort"};
 }
 
 void* Context::scratch_bytes(int slot, size_t bytes) {
@@ -40,6 +45,8 @@ void* Context::scratch_bytes(int slot, size_t bytes) {
 }
 
 void Context::phase_begin(int ph) {
+  nvtxRangePushA(kPhaseName[ph]);
+  nvtx_open = true;
   if (!phase_timing) return;
   if (ev_used + 2 > ev_pool.size()) {
     for (int k = 0; k < 64; ++k) {
@@ -55,6 +62,10 @@ void Context::phase_begin(int ph) {
 }
 
 void Context::phase_end() {
+  if (nvtx_open) {
+    nvtxRangePop();
+    nvtx_open = false;
+  }
   if (!phase_timing || phase_open < 0) return;
   CUDA_OK(cudaEventRecord(ev_pool[(size_t)ev_marks.back().second + 1], stream));
   phase_open = -1;
@@ -1105,6 +1116,10 @@ int pic_diagnostics(pic_context* ctx, pic_diag* out, float* kinetic, size_t kine
     out->max_div_b_err = max_abs_lane(c, F_DIVB);
     out->particle_count = count;
   });
+}
+
+int pic_diagnostics_order(pic_context* ctx, int reference_order) {
+  return guard([&] { C_(ctx).reference_order_sums = reference_order != 0; });
 }
 
 int pic_event_record(pic_context* ctx, int slot) {

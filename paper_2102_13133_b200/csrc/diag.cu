@@ -12,10 +12,19 @@
 //   kinetic_energy            src/particles.cpp:460-466 (+ kinetic_sum, scalar.cpp:61-71)
 //
 // Parity: compute_div_errors and max_abs_lane are bit-exact (a stencil and an
-// order-free max).  The sums (energies, rho) are reassociated — the
-// reference itself changes them with its SIMD lane count and worker count —
-// so they are accumulated in fp64 on the device (energies) or with float
-// atomics (rho) and checked against the oracle within a stated tolerance.
+// order-free max).  The energies have two modes (pic_diagnostics_order):
+//   * fast (default): fp64 device sums of the reference's fp32 terms;
+//   * reference order (deterministic decks): the reference's own fp32
+//     summation — field energy as the serial sum over (lane, z, y) lines of
+//     each line's 8 interleaved partials collapsed pairwise (sum_squares,
+//     kernels/scalar.cpp:51-59, impl.hpp:24-28; the AVX2 lane sums the same
+//     partials, avx2.cpp:192-205), kinetic energy as 8 interleaved partials
+//     over the particles in their order, collapsed pairwise
+//     (particles.cpp:468-501) — bit-identical to the reference.  The 8
+//     partial chains are serial by definition: ~n/8 dependent adds.
+// rho: float atomics (fast), or in reference-order mode the reference's
+// serial order (every node's contributions sorted stably by node, added in
+// particle order) — bit-identical.
 // Per-particle / per-voxel terms keep the reference's fp32 expressions.
 #include <algorithm>
 #include <cstring>
@@ -224,6 +233,129 @@ kinetic_kernel(const float4* __restrict__ pos, const float4* __restrict__ mom, l
   block_add2(acc, 0.0, out);
 }
 
+// sum_squares of one x line (interior ix = 1..nx) per thread, for lanes
+// lane0..lane0+2: the reference's 8 interleaved partials, collapsed pairwise.
+__global__ void __launch_bounds__(128)
+line_sum_squares_kernel(GridC g, const float* __restrict__ f, int lane0, float* __restrict__ out) {
+  const long long lines = 3LL * g.ny * g.nz;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= lines) return;
+  const int l = (int)(t / ((long long)g.ny * g.nz));
+  const long long r = t - (long long)l * g.ny * g.nz;
+  const int iz = 1 + (int)(r / g.ny), iy = 1 + (int)(r % g.ny);
+  const float* x = f + (size_t)(lane0 + l) * (size_t)g.V + (size_t)voxel_of(g, 1, iy, iz);
+  float p[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int k = 0; k < g.nx; ++k) {
+    const float v = x[k];
+    p[k & 7] = p[k & 7] + v * v;
+  }
+#pragma unroll
+  for (int h = 4; h > 0; h >>= 1)
+#pragma unroll
+    for (int j = 0; j < h; ++j) p[j] = p[j] + p[j + h];
+  out[t] = p[0];
+}
+
+// se / sb: the serial fp32 sums over the lines in (lane, z, y) order.
+__global__ void serial_line_sum_kernel(const float* __restrict__ lines, long long n, float* __restrict__ out) {
+  if (threadIdx.x >= 2) return;
+  const float* x = lines + (size_t)threadIdx.x * (size_t)n;
+  float s = 0.f;
+  for (long long i = 0; i < n; ++i) s = s + x[i];
+  out[threadIdx.x] = s;
+}
+
+// kinetic_energy_centered's per-particle terms, in particle order.
+__global__ void __launch_bounds__(256)
+kinetic_terms_kernel(const float4* __restrict__ pos, const float4* __restrict__ mom, long long n,
+                     const float4* __restrict__ interp, float qdt_2m, float m, float* __restrict__ term) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float4 u = mom[i];
+  const float4 p = pos[i];
+  const float4* c = interp + (size_t)__float_as_int(p.w) * kInterpF4;
+  const float4 c0 = __ldg(c), c1 = __ldg(c + 1), c2 = __ldg(c + 2);
+  const float x = p.x, y = p.y, z = p.z;
+  const float ex = ((c0.x + y * c0.y) + z * c0.z) + (y * z) * c0.w;
+  const float ey = ((c1.x + z * c1.y) + x * c1.z) + (z * x) * c1.w;
+  const float ez = ((c2.x + x * c2.y) + y * c2.z) + (x * y) * c2.w;
+  const float cx = u.x + qdt_2m * ex, cy = u.y + qdt_2m * ey, cz = u.z + qdt_2m * ez;
+  const float gm = __fsqrt_rn(1.0f + ((cx * cx + cy * cy) + cz * cz));
+  term[i] = (u.w * m) * (gm - 1.0f);
+}
+
+// p[i % 8] += term[i] in particle order (8 serial chains), collapsed pairwise.
+__global__ void partials8_kernel(const float* __restrict__ term, long long n, float* __restrict__ out) {
+  __shared__ float p[8];
+  const int j = threadIdx.x;
+  if (j < 8) {
+    float s = 0.f;
+    long long i = j;
+    for (; i + 24 < n; i += 32) {  // four loads in flight, the adds in order
+      const float a = term[i], b = term[i + 8], cc = term[i + 16], dd = term[i + 24];
+      s = s + a;
+      s = s + b;
+      s = s + cc;
+      s = s + dd;
+    }
+    for (; i < n; i += 8) s = s + term[i];
+    p[j] = s;
+  }
+  __syncthreads();
+  if (j == 0) {
+    float q[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) q[k] = p[k];
+#pragma unroll
+    for (int h = 4; h > 0; h >>= 1)
+#pragma unroll
+      for (int k = 0; k < h; ++k) q[k] = q[k] + q[k + h];
+    out[0] = q[0];
+  }
+}
+
+// deposit_rho in the reference's order (particles.cpp:384-410): every
+// particle's 8 node contributions, emitted in (particle, corner) order ...
+__global__ void __launch_bounds__(256)
+emit_rho_kernel(GridC g, const float4* __restrict__ pos, const float4* __restrict__ mom, long long i0,
+                long long n, float q, float scale, unsigned* __restrict__ key, float* __restrict__ w) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const float4 p = pos[i0 + t];
+  const float4 u = mom[i0 + t];
+  const int v = __float_as_int(p.w);
+  const unsigned rest = fast_div((unsigned)v, g.mag_pnx);
+  const int ix = v - (int)rest * g.pnx;
+  const unsigned izu = fast_div(rest, g.mag_pny);
+  const int iy = (int)rest - (int)izu * g.pny, iz = (int)izu;
+  const int xh = ix + 1 > g.nx ? 1 : ix + 1, yh = iy + 1 > g.ny ? 1 : iy + 1, zh = iz + 1 > g.nz ? 1 : iz + 1;
+  const float qw = (q * u.w) * scale;
+  const float wxl = 1 - p.x, wxh = 1 + p.x, wyl = 1 - p.y, wyh = 1 + p.y, wzl = 1 - p.z, wzh = 1 + p.z;
+  unsigned* k = key + 8 * t;
+  float* o = w + 8 * t;
+  k[0] = (unsigned)voxel_of(g, ix, iy, iz);  o[0] = qw * (wxl * wyl * wzl);
+  k[1] = (unsigned)voxel_of(g, xh, iy, iz);  o[1] = qw * (wxh * wyl * wzl);
+  k[2] = (unsigned)voxel_of(g, ix, yh, iz);  o[2] = qw * (wxl * wyh * wzl);
+  k[3] = (unsigned)voxel_of(g, xh, yh, iz);  o[3] = qw * (wxh * wyh * wzl);
+  k[4] = (unsigned)voxel_of(g, ix, iy, zh);  o[4] = qw * (wxl * wyl * wzh);
+  k[5] = (unsigned)voxel_of(g, xh, iy, zh);  o[5] = qw * (wxh * wyl * wzh);
+  k[6] = (unsigned)voxel_of(g, ix, yh, zh);  o[6] = qw * (wxl * wyh * wzh);
+  k[7] = (unsigned)voxel_of(g, xh, yh, zh);  o[7] = qw * (wxh * wyh * wzh);
+}
+
+// ... sorted stably by node, then added onto each node in that order.
+__global__ void __launch_bounds__(256)
+ordered_rho_kernel(const unsigned* __restrict__ start, const unsigned* __restrict__ idx,
+                   const float* __restrict__ w, float* __restrict__ rho, long long V) {
+  const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  const unsigned b = start[v], e = start[v + 1];
+  if (b == e) return;
+  float r = rho[v];
+  for (unsigned t = b; t < e; ++t) r = r + w[idx[t]];
+  rho[v] = r;
+}
+
 unsigned grid_stride_blocks(const Context& c, long long n) {
   const long long want = (n + 255) / 256;
   const long long cap = (long long)c.num_sms * 8;
@@ -239,6 +371,28 @@ void launch_clear_rho(Context& c) {
 void launch_deposit_rho(Context& c, Species& s) {
   if (s.n == 0) return;
   const float scale = 0.125f / ((c.grid.hx * c.grid.hy) * c.grid.hz);
+  if (c.reference_order_sums && !s.ordered) {
+    // the reference's serial order, in chunks of particles (8 contributions
+    // each; a chunk's node sums continue the previous chunk's)
+    const long long V = c.gc.V;
+    const long long chunk = 1LL << 26;
+    for (long long i0 = 0; i0 < (long long)s.n; i0 += chunk) {
+      const long long n = std::min<long long>(chunk, (long long)s.n - i0);
+      unsigned* key = static_cast<unsigned*>(c.scratch_bytes(Context::kScrSegKey, (size_t)(8 * n) * 4));
+      float* w = static_cast<float*>(c.scratch_bytes(Context::kScrSegW, (size_t)(8 * n) * 4));
+      emit_rho_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(c.gc, s.pos, s.mom, i0, n, s.q, scale,
+                                                                       key, w);
+      c.count_launch();
+      unsigned *skey = nullptr, *sval = nullptr;
+      radix_sort_pairs(c, key, nullptr, (size_t)(8 * n), key_bits_for(V), &skey, &sval);
+      unsigned* start = static_cast<unsigned*>(c.scratch_bytes(Context::kScrStart, (size_t)(V + 1) * 4));
+      key_run_starts(c, skey, (size_t)(8 * n), (size_t)V, start);
+      ordered_rho_kernel<<<(unsigned)((V + 255) / 256), 256, 0, c.stream>>>(start, sval, w,
+                                                                          c.f + (size_t)F_RHO * c.gc.V, V);
+      c.count_launch();
+    }
+    return;
+  }
   deposit_rho_kernel<<<(unsigned)((s.n + 255) / 256), 256, 0, c.stream>>>(
       c.gc, s.pos, s.mom, (long long)s.n, s.q, scale, c.f + (size_t)F_RHO * c.gc.V);
   c.count_launch();
@@ -256,6 +410,22 @@ double* diag_slots(Context& c) {
 }
 
 void field_energy(Context& c, float e_b[2]) {
+  if (c.reference_order_sums) {
+    // field_energy (fields.cpp:276-299) in the reference's summation order
+    const long long lines = 3LL * c.gc.ny * c.gc.nz;
+    float* ls = static_cast<float*>(c.scratch_bytes(Context::kScrDiagLines, (size_t)(2 * lines + 2) * sizeof(float)));
+    line_sum_squares_kernel<<<(unsigned)((lines + 127) / 128), 128, 0, c.stream>>>(c.gc, c.f, F_EX, ls);
+    line_sum_squares_kernel<<<(unsigned)((lines + 127) / 128), 128, 0, c.stream>>>(c.gc, c.f, F_BX, ls + lines);
+    serial_line_sum_kernel<<<1, 32, 0, c.stream>>>(ls, lines, ls + 2 * lines);
+    c.count_launch(3);
+    float h[2];
+    CUDA_OK(cudaMemcpyAsync(h, ls + 2 * lines, sizeof h, cudaMemcpyDeviceToHost, c.stream));
+    CUDA_OK(cudaStreamSynchronize(c.stream));
+    const float hv = 0.5f * ((c.grid.hx * c.grid.hy) * c.grid.hz);
+    e_b[0] = hv * h[0];
+    e_b[1] = hv * h[1];
+    return;
+  }
   double* d = diag_slots(c);
   CUDA_OK(cudaMemsetAsync(d, 0, 2 * sizeof(double), c.stream));
   const long long n = (long long)c.gc.nx * c.gc.ny * c.gc.nz;
@@ -285,6 +455,19 @@ float max_abs_lane(Context& c, int lane) {
 
 float kinetic_energy(Context& c, Species& s, bool centered) {
   if (s.n == 0) return 0.0f;
+  if (c.reference_order_sums && centered && !s.ordered) {
+    // kinetic_energy_centered (particles.cpp:468-501) in the reference's order
+    float* term = static_cast<float*>(c.scratch_bytes(Context::kScrDiagLines, (s.n + 8) * sizeof(float)));
+    const float qdt_2m = (s.q * c.grid.dt) / (2.0f * s.m);
+    kinetic_terms_kernel<<<(unsigned)((s.n + 255) / 256), 256, 0, c.stream>>>(s.pos, s.mom, (long long)s.n,
+                                                                             c.interp, qdt_2m, s.m, term);
+    partials8_kernel<<<1, 32, 0, c.stream>>>(term, (long long)s.n, term + s.n);
+    c.count_launch(2);
+    float h = 0.f;
+    CUDA_OK(cudaMemcpyAsync(&h, term + s.n, sizeof h, cudaMemcpyDeviceToHost, c.stream));
+    CUDA_OK(cudaStreamSynchronize(c.stream));
+    return h;
+  }
   double* d = diag_slots(c) + 16;
   CUDA_OK(cudaMemsetAsync(d, 0, 2 * sizeof(double), c.stream));
   const float qdt_2m = (s.q * c.grid.dt) / (2.0f * s.m);

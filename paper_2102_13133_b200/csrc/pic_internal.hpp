@@ -100,6 +100,7 @@ struct Context {
   int sort_radix_bits = 9;  // LSD digit width (passes = ceil(key bits / width), widths evened out)
   int sort_match = 1;       // group equal digits with match.any (0: per-bit ballots)
   bool sort_defer = true;   // blocked sorts leave the permutation to the next push
+  bool reference_order_sums = false;  // energies in the reference's fp32 order (pic_diagnostics_order)
   bool voxel_order = true;  // fast periodic pushes keep the store near voxel order (order.cu)
   int reorder_interval = 5;  // every m-th ordered push reorders the store (PIC_REORDER_INTERVAL)
   int num_sms = 148;
@@ -147,7 +148,7 @@ struct Context {
     kScrStage = 0, kScrNseg, kScrOff, kScrSegKey, kScrSegW,
     kScrKeyA, kScrValA, kScrKeyB, kScrValB, kScrHist, kScrScan,
     kScrCount, kScrStart, kScrWithin, kScrStaging, kScrSmall, kScrDiag, kScrMigA, kScrMigB, kScrMigC, kScrMigT,
-    kScrWall, kScrN
+    kScrWall, kScrDiagLines, kScrN
   };
   void* scratch[kScrN] = {};
   size_t scratch_size[kScrN] = {};
@@ -161,6 +162,7 @@ struct Context {
   size_t ev_used = 0;
   double phase_ms[kPhN] = {};
   int phase_open = -1;
+  bool nvtx_open = false;  // an NVTX phase range is pushed
   void phase_begin(int ph);
   void phase_end();
   void resolve_phases();

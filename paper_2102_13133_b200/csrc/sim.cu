@@ -407,6 +407,20 @@ struct Sim {
   Context* ctx = nullptr;
   long step_count = 0;
   std::vector<std::string> warnings;
+  // hooks (sim.hpp:102-127) and their host mirrors (allocated on first use)
+  struct Hook {
+    std::string name;
+    long interval;
+    pic_hook_flags flags;
+    pic_hook_fn fn;
+    void* user;
+  };
+  std::vector<Hook> hooks;
+  std::vector<float> host_fields;
+  std::vector<std::vector<float>> host_lanes;
+  std::vector<std::vector<int32_t>> host_ids;
+  uint64_t copies = 0;
+  pic_sim* handle = nullptr;
   bool header_done = false;
   std::chrono::steady_clock::time_point last_wall;
   long last_step = 0;
@@ -423,6 +437,9 @@ struct Sim {
   // SimState::initialize (proj/src/sim.cpp:74-134)
   Sim(int device, const Deck& d) : deck(d), grid(deck_grid(d)) {
     ctx = make_context(device, grid);
+    // deterministic decks: energies in the reference's fp32 summation order,
+    // so the diagnostics CSV is the reference's byte for byte
+    ctx->reference_order_sums = deck.deterministic;
     try {
       const size_t interior = (size_t)grid.nx * grid.ny * grid.nz;
       const float hx = grid.hx, lx = grid.hx * (float)grid.nx;
@@ -571,7 +588,62 @@ struct Sim {
     if (!out) throw RunAbort("dump_fields: write failed for " + path);
   }
 
-  // SimState::run (sim.cpp:285-306), hooks excepted
+  // SimState::run_hooks (sim.cpp:190-215): mirrors refreshed / copied back
+  // per the hook's flags, one counted copy per species or field array
+  void run_hooks() {
+    for (auto& h : hooks) {
+      if (step_count == 0 || step_count % h.interval != 0) continue;
+      const size_t ns = ctx->species.size();
+      host_lanes.resize(ns);
+      host_ids.resize(ns);
+      const size_t V = (size_t)ctx->gc.V;
+      if (host_fields.size() != F_COUNT * V) host_fields.assign(F_COUNT * V, 0.f);
+      std::vector<size_t> counts(ns);
+      for (size_t i = 0; i < ns; ++i) {
+        counts[i] = ctx->species[i].n;
+        if (host_lanes[i].size() != 7 * counts[i]) host_lanes[i].assign(7 * counts[i], 0.f);
+        if (host_ids[i].size() != counts[i]) host_ids[i].assign(counts[i], 0);
+      }
+      pic_context view_ctx{ctx, true};
+      if (h.flags.particles_to_host)
+        for (size_t i = 0; i < ns; ++i) {
+          if (int rc = pic_species_download(&view_ctx, (int)i, host_lanes[i].data(), host_ids[i].data()))
+            throw RunAbort(std::string("run_hooks: particle mirror: ") + pic_last_error() + " (" +
+                           std::to_string(rc) + ")");
+          ++copies;
+        }
+      if (h.flags.fields_to_host) {
+        if (pic_fields_download(&view_ctx, host_fields.data())) throw RunAbort(pic_last_error());
+        ++copies;
+      }
+      if (h.fn) {
+        std::vector<float*> lp(ns);
+        std::vector<int32_t*> ip(ns);
+        for (size_t i = 0; i < ns; ++i) {
+          lp[i] = host_lanes[i].data();
+          ip[i] = host_ids[i].data();
+        }
+        pic_hook_view v{handle, step_count, host_fields.data(), ns, lp.data(), ip.data(), counts.data()};
+        const int rc = h.fn(&v, h.user);
+        if (rc != 0)
+          throw RunAbort("hook '" + h.name + "' failed at step " + std::to_string(step_count) +
+                         ": callback returned " + std::to_string(rc));
+      }
+      if (h.flags.particles_back)
+        for (size_t i = 0; i < ns; ++i) {
+          if (int rc = pic_species_upload(&view_ctx, (int)i, counts[i], host_lanes[i].data(), host_ids[i].data()))
+            throw RunAbort(std::string("run_hooks: particle copy-back: ") + pic_last_error() + " (" +
+                           std::to_string(rc) + ")");
+          ++copies;
+        }
+      if (h.flags.fields_back) {
+        if (pic_fields_upload(&view_ctx, host_fields.data())) throw RunAbort(pic_last_error());
+        ++copies;
+      }
+    }
+  }
+
+  // SimState::run (sim.cpp:285-306)
   void run(std::ostream* csv) {
     namespace fs = std::filesystem;
     if (deck.field_dump_interval > 0) fs::create_directories(deck.out_dir);
@@ -581,6 +653,7 @@ struct Sim {
       sort_due();
       const bool due = step_count % deck.diag_interval == 0;
       if (due) refresh_charge();
+      run_hooks();
       if (due && csv) *csv << diagnostics_row();
       if (deck.field_dump_interval > 0 && step_count % deck.field_dump_interval == 0)
         dump_fields((fs::path(deck.out_dir) / ("fields_" + std::to_string(step_count) + ".bin")).string());
@@ -667,6 +740,7 @@ int pic_sim_create(int device, const pic_deck* d, pic_sim** out) {
     *out = nullptr;
     Sim* s = new Sim(device, d->d);
     *out = new pic_sim{s, new pic_context{s->ctx, true}};
+    s->handle = *out;
   });
 }
 int pic_sim_destroy(pic_sim* s) {
@@ -717,6 +791,18 @@ int pic_sim_run(pic_sim* s, const char* csv_path) {
 }
 int pic_sim_dump_fields(pic_sim* s, const char* path) {
   return capi_guard([&] { S_(s).dump_fields(path); });
+}
+int pic_sim_register_hook(pic_sim* s, const char* name, long interval, const pic_hook_flags* flags,
+                          pic_hook_fn fn, void* user) {
+  return capi_guard([&] {
+    Sim& m = S_(s);
+    if (interval < 1) throw UsageError("register_hook: interval must be >= 1");
+    const pic_hook_flags legacy{1, 1, 1, 1};
+    m.hooks.push_back({name ? name : "hook", interval, flags ? *flags : legacy, fn, user});
+  });
+}
+int pic_sim_copies_performed(pic_sim* s, uint64_t* out) {
+  return capi_guard([&] { *out = S_(s).copies; });
 }
 int pic_sim_warnings(pic_sim* s, char* buf, size_t cap, size_t* len) {
   return capi_guard([&] {

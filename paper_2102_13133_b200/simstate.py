@@ -10,7 +10,49 @@ from __future__ import annotations
 
 import ctypes as C
 
+import numpy as np
+
 from . import Context, Grid, check, lib
+
+
+class HookFlags(C.Structure):
+    """HookFlags (proj/include/minipic/sim.hpp:102-110)."""
+    _fields_ = [("particles_to_host", C.c_int), ("fields_to_host", C.c_int), ("particles_back", C.c_int),
+                ("fields_back", C.c_int)]
+
+    @classmethod
+    def legacy(cls):
+        return cls(1, 1, 1, 1)
+
+    @classmethod
+    def none(cls):
+        return cls(0, 0, 0, 0)
+
+
+class _HookView(C.Structure):
+    _fields_ = [("sim", C.c_void_p), ("step", C.c_long), ("fields16", C.POINTER(C.c_float)),
+                ("nspecies", C.c_size_t), ("lanes7", C.POINTER(C.POINTER(C.c_float))),
+                ("ids", C.POINTER(C.POINTER(C.c_int32))), ("counts", C.POINTER(C.c_size_t))]
+
+
+_HOOK_FN = C.CFUNCTYPE(C.c_int, C.POINTER(_HookView), C.c_void_p)
+
+
+class HookContext:
+    """HookContext (sim.hpp:113-119): the step and the host mirrors as numpy
+    views (fields (16, V), per species lanes (7, n) and ids (n,)); writes go
+    back to the device when the hook's flags say so."""
+
+    def __init__(self, sim, v, padded):
+        self.state = sim
+        self.step = v.step
+        self.host_fields = np.ctypeslib.as_array(v.fields16, shape=(16, padded))
+        self.host_particles = []
+        for i in range(v.nspecies):
+            n = v.counts[i]
+            lanes = np.ctypeslib.as_array(v.lanes7[i], shape=(7, n)) if n else np.zeros((7, 0), np.float32)
+            ids = np.ctypeslib.as_array(v.ids[i], shape=(n,)) if n else np.zeros(0, np.int32)
+            self.host_particles.append((lanes, ids))
 
 
 class Deck:
@@ -97,6 +139,37 @@ class SimState:
     def step(self):
         """SimState::step + sort_due_species."""
         check(lib().pic_sim_step(self._h))
+
+    def register_hook(self, action, interval=1, flags=None, name="hook"):
+        """SimState::register_hook (sim.cpp:185-188): action(HookContext) runs
+        in run() every interval steps; an exception in it aborts the run."""
+        padded = self.deck.grid().padded
+        errors = []
+
+        def trampoline(view, user):
+            try:
+                if action is not None:
+                    action(HookContext(self, view.contents, padded))
+                return 0
+            except Exception as e:  # reported by the C side as run_abort
+                errors.append(e)
+                return 1
+
+        cb = _HOOK_FN(trampoline)
+        if not hasattr(self, "_hooks"):
+            self._hooks = []
+        self._hooks.append((cb, errors))
+        fn = lib().pic_sim_register_hook
+        fn.argtypes = [C.c_void_p, C.c_char_p, C.c_long, C.POINTER(HookFlags), _HOOK_FN, C.c_void_p]
+        check(fn(self._h, name.encode(), int(interval), C.byref(flags) if flags is not None else None, cb, None))
+
+    def copies_performed(self) -> int:
+        """SimState::copies_performed (sim.hpp:175)."""
+        out = C.c_uint64()
+        fn = lib().pic_sim_copies_performed
+        fn.argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
+        check(fn(self._h, C.byref(out)))
+        return out.value
 
     @property
     def step_count(self) -> int:

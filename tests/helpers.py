@@ -62,3 +62,16 @@ def assert_close(a, b, rtol, atol_scale=None, what=""):
     scale = atol_scale if atol_scale is not None else max(np.abs(b).max(), 1e-30)
     err = np.abs(a - b).max() if a.size else 0.0
     assert err <= rtol * scale, f"{what}: max |diff| {err:.3e} > {rtol:g} * {scale:.3e}"
+
+
+def rel_err_percentiles(a, b, floor_frac=1e-3):
+    """Per-element relative error |a - b| / (|b| + floor), floor = floor_frac x
+    rms(b) (elements at the array's zero crossings are compared at that
+    floor), as (p50, p99, max)."""
+    a = np.asarray(a, np.float64).ravel()
+    b = np.asarray(b, np.float64).ravel()
+    if a.size == 0:
+        return 0.0, 0.0, 0.0
+    floor = floor_frac * max(float(np.sqrt(np.mean(b * b))), 1e-30)
+    e = np.abs(a - b) / (np.abs(b) + floor)
+    return float(np.percentile(e, 50)), float(np.percentile(e, 99)), float(e.max())

@@ -1,0 +1,100 @@
+"""Hooks with residency flags and copy counting:
+HookRegistration / HookFlags / run_hooks (proj/include/minipic/sim.hpp:
+102-127, proj/src/sim.cpp:185-215), and the reference's acceptance
+criterion 12 (proj/tests/acceptance.cpp:727-784): a hook with empty flags
+costs no copies, the legacy flags cost 2 x species + 2 per invocation."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+DECK = """[grid]
+nx = 6
+ny = 6
+nz = 6
+lx = 6
+ly = 6
+lz = 6
+dt = 0.1
+steps = 10
+
+[species.electron]
+q = -1
+m = 1
+ppc = 2
+
+[species.positron]
+q = 1
+m = 1
+ppc = 2
+
+[run]
+seed = 77
+"""
+
+
+def _sim(text=DECK):
+    from paper_2102_13133_b200.simstate import Deck, SimState
+    return SimState(Deck(text))
+
+
+def test_hook_residency_accounting():
+    from paper_2102_13133_b200.simstate import HookFlags
+    with _sim() as s:
+        seen = []
+        s.register_hook(lambda h: seen.append(h.step), interval=5, flags=HookFlags.none(), name="empty")
+        before = s.copies_performed()
+        s.run()
+        assert s.copies_performed() == before  # empty flags: no copies
+        assert seen == [5, 10]
+    with _sim() as s:
+        s.register_hook(lambda h: None, interval=5, name="legacy")
+        before = s.copies_performed()
+        s.run()
+        assert s.copies_performed() - before == 2 * (2 + 2 + 1 + 1)  # criterion 12: 12
+
+
+def test_hook_sees_and_writes_back_state():
+    """The mirrors are the device state in the reference's order; writes go
+    back with particles_back / fields_back and only then."""
+    from paper_2102_13133_b200.simstate import HookFlags
+    with _sim(DECK.replace("steps = 10", "steps = 4")) as s:
+        got = {}
+
+        def look(h):
+            lanes, ids = h.host_particles[0]
+            got["n"] = lanes.shape[1]
+            got["ids"] = ids.copy()
+            lanes[3:6] = 0.0  # stop species 0
+            h.host_fields[4] = 0.25  # B_x everywhere
+
+        s.register_hook(look, interval=2, flags=HookFlags(1, 1, 1, 1))
+        s.run()
+        p, ids = s.context.download_species(0)
+        f = s.context.download_fields()
+    assert got["n"] == 6 ** 3 * 2
+    # after the hook at step 4 (the last) the momenta stay zeroed and B_x = 0.25
+    assert (p[3:6] == 0).all()
+    assert (f[4] == np.float32(0.25)).all()
+    warm = DECK.replace("steps = 10", "steps = 4").replace("ppc = 2\n\n[species.positron]", "ppc = 2\nu_th = 0.1\n\n[species.positron]")
+    with _sim(warm) as s:
+        def poke(h):
+            h.host_particles[0][0][3:6] = 0.0
+
+        s.register_hook(poke, interval=2, flags=HookFlags(1, 0, 0, 0))  # no copy back
+        s.run()
+        p, _ = s.context.download_species(0)
+    assert (p[3:6] != 0).any()
+
+
+def test_hook_failure_is_run_abort_and_bad_interval_usage_error():
+    import paper_2102_13133_b200 as pic
+    with _sim() as s:
+        def boom(h):
+            raise ValueError("no")
+        s.register_hook(boom, interval=3, name="bad")
+        with pytest.raises(pic.RunAbort, match="hook 'bad' failed at step 3"):
+            s.run()
+    with _sim() as s:
+        with pytest.raises(pic.UsageError, match="interval must be >= 1"):
+            s.register_hook(lambda h: None, interval=0)

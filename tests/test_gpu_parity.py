@@ -11,7 +11,7 @@ ACC_RTOL x max|acc|.
 import numpy as np
 import pytest
 
-from tests.helpers import assert_bitwise, assert_close, rand_fields, rand_particles
+from tests.helpers import assert_bitwise, assert_close, rand_fields, rand_particles, rel_err_percentiles
 
 pytestmark = pytest.mark.gpu
 
@@ -333,11 +333,17 @@ def test_full_step_parity(pic, orc, deterministic):
                 else:
                     assert (gids == ids).mean() > 0.999
                     assert_close(gp[3:6], p[3:6], 1e-4, what=f"step {k} momenta")
+                    # per element (north_star: 1e-5 per step): the median and the
+                    # 99th percentile of the relative error grow at most 1e-5 / step
+                    p50, p99, pmax = rel_err_percentiles(gp[:6], p[:6])
+                    assert p50 <= 1e-5 * k and p99 <= 1e-5 * k, (k, "offsets/momenta", p50, p99, pmax)
             if deterministic:
                 assert_bitwise(gf, f, f"step {k} fields")
             else:
                 for lane in (0, 1, 2, 4, 5, 6, 8, 9, 10):
                     assert_close(gf[lane], f[lane], 1e-4, what=f"step {k} lane {lane}")
+                    p50, p99, pmax = rel_err_percentiles(gf[lane], f[lane])
+                    assert p50 <= 1e-5 * (k + 1) and p99 <= 1e-5 * (k + 1), (k, lane, p50, p99, pmax)
 
 
 def test_step_host_matches_device_step(pic, orc):
