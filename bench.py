@@ -363,10 +363,157 @@ def run_ours(args, rank, world):
 
 
 def run_ours_decomposed(args, rank, world):
-    """N > 1: weak-scaled slab decomposition.  The global box is
-    (n N) x n x n with each rank's slab the single-GPU deck; particles
-    migrate, the accumulator is halo-added and E/B halos copied over NCCL
-    (paper_2102_13133_b200/domain.py) every step."""
+    """N > 1 (or --decomposed): weak-scaled slab decomposition.
+    The global box is (n N) x n x n with each rank's slab the single-GPU
+    deck.  Periodic decks run the C++ decomposed step (pic_dd: pushes, fold,
+    fields and the migration / halo exchanges as NCCL send / receive inside
+    the library, graph-captured, no host synchronisation); the walled LPI
+    deck runs the host-sequenced exchanges of domain.py."""
+    import torch
+
+    import paper_2102_13133_b200 as pic
+    from paper_2102_13133_b200.domain import SlabGeometry
+
+    torch.cuda.set_device(args.device)
+    cfg = CONFIGS[args.config]
+    deck = cfg.get("deck")
+    if deck is not None and hasattr(deck, "laser_ix"):
+        return run_ours_decomposed_py(args, rank, world)
+    n = cfg["n"]
+    if deck:  # weak scaling: the global box grows in x, (nx N) x ny x nz
+        import dataclasses
+        NX0 = deck.n[0]
+        deck = dataclasses.replace(deck, n=(NX0 * world, deck.n[1], deck.n[2]))
+        geom = SlabGeometry(*deck.n, world, h=(cfg["h"],) * 3, dt=cfg["dt"])
+    else:
+        geom = SlabGeometry(n * world, n, n, world, h=(cfg["h"],) * 3, dt=cfg["dt"])
+    g = geom.local_grid()
+    ctx = pic.Context(g, device=args.device)
+    ctx.set_x_open(True, rank == 0)
+    sids = []
+    if deck:
+        for name, q, m, uth, drift, sheet in deck.species():
+            sid = ctx.add_species(name, q, m, int(deck.ppc * g.interior * 1.02) + 65536)
+            ctx.load_harris(sid, deck.ppc, uth, drift, seed=1234 + 7919 * rank, **sheet)
+            sids.append(sid)
+        ctx.upload_fields(deck.fields(g, x0=geom.x0(rank)))
+    else:
+        for name, q, m, ppc, uth, drift in cfg["species"]:
+            sid = ctx.add_species(name, q, m, int(ppc * g.interior * 1.02) + 65536)
+            ctx.load_synthetic(sid, ppc, uth, drift, seed=1234 + 7919 * rank)
+            sids.append(sid)
+    import torch.distributed as dist
+    uid = [pic.dd_unique_id() if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(uid, src=0)
+    dd = pic.DecomposedStep(ctx, rank, world, uid[0])
+    ctx.synchronize()
+    sort_interval = cfg["sort_interval"]
+    step_count = [0]
+
+    def one_step():
+        dd.step()
+        step_count[0] += 1
+        if sort_interval > 0 and step_count[0] % sort_interval == 0:
+            for s_ in sids:
+                ctx.sort_particles(s_)
+
+    for s_ in sids:
+        ctx.sort_particles(s_)
+    for _ in range(args.warmup):
+        one_step()
+    ctx.synchronize()
+    clocks = ClockSampler(args.device)
+    clocks.start()
+    dist.barrier()
+    ctx.synchronize()
+    l0 = ctx.launch_count()
+    ctx.event(0)
+    for _ in range(args.steps):
+        one_step()
+    ctx.event(1)
+    ctx.synchronize()
+    dist.barrier()
+    ms = ctx.elapsed_ms(0, 1)
+    launches = ctx.launch_count() - l0
+    clk = clocks.stop()
+    # phase split (the same steps again, plain launches with PhaseTimings events)
+    ctx.phase_timing(True)
+    ctx.phase_timings(reset=True)
+    for _ in range(args.steps):
+        one_step()
+    ctx.synchronize()
+    ph = ctx.phase_timings(reset=True)
+    ctx.phase_timing(False)
+    npart_local = sum(ctx.species_count(s_) for s_ in sids)
+    t = torch.tensor([ms, float(npart_local), ph["push"]], dtype=torch.float64, device="cuda")
+    mx = t.clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    sm = t.clone()
+    dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+    ms = float(mx[0].item())
+    npart_total = int(sm[1].item())
+    push_ms_per_launch = float(mx[2].item()) / (args.steps * len(sids))
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e_dd(pic, dd, ctx, sids, args, world)
+    dd.close()
+    ctx.close()
+    return dict(ms=ms, npart=npart_total // world, npart_total=npart_total, launches=launches, clocks=clk,
+                phases=ph, push_rate_kernel=npart_local * args.steps / (ph["push"] / 1e3),
+                push_ms_per_launch=push_ms_per_launch, nspecies=len(sids), grid=geom.global_grid(), e2e=e2e,
+                local_grid=g, decomposed=True, exchange="C++ pic_dd over NCCL (graph-captured)")
+
+
+def run_e2e_dd(pic, dd, ctx, sids, args, world):
+    """Decomposed host-buffer steps: every step uploads each rank's species
+    from pinned host records, runs the decomposed step, downloads them."""
+    import torch
+    import torch.distributed as dist
+    host = []
+    for s_ in sids:
+        cap = ctx.species_count(s_) + (1 << 20)
+        pos = np.zeros((cap, 4), np.float32)
+        mom = np.zeros((cap, 4), np.float32)
+        pic.host_register(pos)
+        pic.host_register(mom)
+        host.append([pos, mom, ctx.download_records(s_, pos, mom)])
+
+    def step():
+        b = 0
+        for s_, h in zip(sids, host):
+            ctx.upload_records(s_, h[0], h[1], h[2])
+            b += 32 * h[2]
+        dd.step()
+        for s_, h in zip(sids, host):
+            h[2] = ctx.download_records(s_, h[0], h[1])
+        return b
+
+    step()
+    dist.barrier()
+    k = max(1, args.e2e_steps)
+    t0 = time.perf_counter()
+    byt = 0
+    for _ in range(k):
+        byt += step()
+    dt = time.perf_counter() - t0
+    t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dt = float(t.item())
+    npart = sum(h[2] for h in host)
+    tn = torch.tensor([float(npart)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(tn)
+    for h in host:
+        pic.host_unregister(h[0])
+        pic.host_unregister(h[1])
+    return {"value": float(tn.item()) * k / dt, "value_per_gpu": float(tn.item()) * k / dt / world,
+            "unit": "particle pushes/s", "h2d_bytes_per_step": byt // k,
+            "d2h_bytes_per_step": byt // k, "steps": k, "ms_per_step": dt / k * 1e3,
+            "note": "per rank: records H2D, decomposed step, records D2H (not pipelined); bytes are rank 0's"}
+
+
+def run_ours_decomposed_py(args, rank, world):
+    """The walled LPI deck: host-sequenced exchanges (domain.py)."""
     import torch
 
     import paper_2102_13133_b200 as pic
@@ -689,6 +836,7 @@ def main():
                    "parallelism": f"x-slab decomposition over {world} GPUs (NCCL halo + migration)"
                    if res.get("decomposed") else "single",
                    "global_cells": f"{g.nx}x{g.ny}x{g.nz}",
+                   **({"exchange": res["exchange"]} if res.get("exchange") else {}),
                    "l2": "inputs (34 GB of particle records) >> 126 MB L2; no flush",
                    "push_kernel_rate": res["push_rate_kernel"],
                    "phase_ms_per_step": {k: v / args.steps for k, v in res["phases"].items()}},

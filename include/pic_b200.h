@@ -326,6 +326,26 @@ int pic_diagnostics(pic_context* ctx, pic_diag* out, float* kinetic, size_t kine
  * n/8 adds.  pic_sim sets 1 for decks with run.deterministic = true. */
 int pic_diagnostics_order(pic_context* ctx, int reference_order);
 
+/* ---- the x-slab decomposed fast step over NCCL --------------
+ * One process per GPU; each owns an x-open context (pic_set_x_open, with
+ * low_wraps on rank 0) for its slab of a global periodic box of world slabs.
+ * pic_dd_step runs SimState::step over the slab with the three x exchanges
+ * of the single-domain wrap — particle migration (particles.cpp:348-350),
+ * the accumulator halo-add (grid.cpp:78-86) and the E / B halo copy
+ * (fields.cpp:35-44) — as grouped ncclSend / ncclRecv on the context stream
+ * with no host synchronisation (counts stay on the device; migration
+ * buffers hold mig_frac x a boundary plane's share of the capacity, 0 =
+ * 1/8; an overflow is a run_abort), captured as a CUDA graph after its first
+ * steps.  Fast mode, periodic boxes; walled decks and deterministic mode use
+ * the host-sequenced exchanges (halo / migrate entry points below).  NCCL
+ * is loaded at run time (the process's libnccl.so.2); world 1 sends to
+ * itself. */
+typedef struct pic_dd pic_dd;
+int pic_dd_unique_id(void* out128); /* ncclGetUniqueId, 128 bytes, on rank 0 */
+int pic_dd_create(pic_context* ctx, int rank, int world, const void* unique_id128, double mig_frac, pic_dd** out);
+int pic_dd_step(pic_dd* dd, unsigned flags);
+int pic_dd_destroy(pic_dd* dd);
+
 /* ---- decks and the SimState run surface ---------------
  * The reference's host API above the step: the deck text format
  * (proj/src/deck.cpp:20-395), SimState::initialize / step / run /

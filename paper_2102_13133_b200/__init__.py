@@ -603,3 +603,46 @@ def host_register(arr: np.ndarray):
 
 def host_unregister(arr: np.ndarray):
     check(lib().pic_host_unregister(arr.ctypes.data))
+
+
+# --- the decomposed fast step in C++ over NCCL (pic_dd) ----------------
+def dd_unique_id() -> bytes:
+    """ncclGetUniqueId (rank 0; broadcast it to the other ranks)."""
+    import torch  # noqa: F401  (loads the process's NCCL; the library binds to it)
+    buf = C.create_string_buffer(128)
+    fn = lib().pic_dd_unique_id
+    fn.argtypes = [C.c_void_p]
+    check(fn(buf))
+    return buf.raw
+
+
+class DecomposedStep:
+    """pic_dd: SimState::step over this rank's x-open slab with the x
+    exchanges (migration, accumulator halo-add, E/B halo) as NCCL send /
+    receive inside the library, no host synchronisation, graph-captured."""
+
+    def __init__(self, ctx: "Context", rank: int, world: int, unique_id: bytes, mig_frac: float = 0.0):
+        import torch  # noqa: F401  (loads the process's NCCL; the library binds to it)
+        self.ctx = ctx
+        self._h = C.c_void_p()
+        fn = lib().pic_dd_create
+        fn.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_char_p, C.c_double, C.POINTER(C.c_void_p)]
+        check(fn(ctx._h, rank, world, unique_id, mig_frac, C.byref(self._h)))
+
+    def step(self, exact_gyration: bool = False):
+        fn = lib().pic_dd_step
+        fn.argtypes = [C.c_void_p, C.c_uint]
+        check(fn(self._h, PIC_EXACT_GYRATION if exact_gyration else 0))
+
+    def close(self):
+        if self._h:
+            fn = lib().pic_dd_destroy
+            fn.argtypes = [C.c_void_p]
+            check(fn(self._h))
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

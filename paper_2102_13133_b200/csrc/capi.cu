@@ -93,6 +93,7 @@ void Context::release() {
     cudaFree(s.pos_alt);
     cudaFree(s.mom_alt);
     cudaFree(s.perm);
+    cudaFree(s.dn);
     cudaFree(s.lidx);
     cudaFree(s.lidx_alt);
     cudaFree(s.vcur);
@@ -236,9 +237,20 @@ void quiesce(Context& c) {
 // A species for an entry point: any deferred sort permutation is applied
 // first (the reference's order is what every caller observes); the push and
 // the count take it as it is (species_ref).
+void settle_count(Context& c, Species& s) {
+  if (!s.n_on_device) return;
+  unsigned long long n = 0;
+  CUDA_OK(cudaMemcpyAsync(&n, s.dn, sizeof n, cudaMemcpyDeviceToHost, c.stream));
+  CUDA_OK(cudaStreamSynchronize(c.stream));
+  s.n = (size_t)n;
+  s.n_on_device = false;
+}
+
 static Species& species_ref(Context& c, int sid) {
   if (sid < 0 || sid >= (int)c.species.size()) throw UsageError("species index out of range");
-  return c.species[(size_t)sid];
+  Species& s = c.species[(size_t)sid];
+  settle_count(c, s);
+  return s;
 }
 Species& species_at(Context& c, int sid) {
   Species& s = species_ref(c, sid);
@@ -290,6 +302,7 @@ static void step_epilogue(Context& c) {
 }
 
 void step(Context& c, unsigned flags) {
+  for (auto& s : c.species) settle_count(c, s);
   const bool det = (flags & PIC_DETERMINISTIC) != 0;
   const bool exact = (flags & PIC_EXACT_GYRATION) != 0;
   const bool walls = has_walls(c);
@@ -822,6 +835,7 @@ static void apply_species_state(Context& c, const std::vector<Context::SpeciesSt
 }
 
 void step_graphed(Context& c, unsigned flags) {
+  for (auto& s : c.species) settle_count(c, s);
   if (!graph_ok(c, flags)) {
     step(c, flags);
     return;
@@ -1059,6 +1073,7 @@ int pic_compute_div_errors(pic_context* ctx) {
 int pic_refresh_charge_diagnostics(pic_context* ctx) {
   return guard([&] {
     Context& c = C_(ctx);
+    for (auto& s : c.species) settle_count(c, s);
     materialize_for_sums(c);
     launch_clear_rho(c);
     for (auto& s : c.species) launch_deposit_rho(c, s);
@@ -1094,6 +1109,7 @@ int pic_diagnostics(pic_context* ctx, pic_diag* out, float* kinetic, size_t kine
   return guard([&] {
     Context& c = C_(ctx);
     if (!out) throw UsageError("diagnostics: null output");
+    for (auto& s : c.species) settle_count(c, s);
     materialize_for_sums(c);
     if (kinetic_cap < c.species.size() || (!kinetic && !c.species.empty()))
       throw UsageError("diagnostics: kinetic[] smaller than the species count");

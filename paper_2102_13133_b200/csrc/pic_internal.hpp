@@ -59,6 +59,11 @@ struct Species {
   // other consumer materialises it first (materialize()).
   unsigned* perm = nullptr;  // cap entries (lazy)
   bool perm_pending = false;
+  // the decomposed C++ step (dd.cu) keeps the count on the device across
+  // its migrations: dn is authoritative while n_on_device (s.n stale);
+  // species_ref() settles it back to the host
+  unsigned long long* dn = nullptr;
+  bool n_on_device = false;
   // Voxel order of the fast push's store (order.cu): physical record i is
   // logical (reference-order) record lidx[i]; vcnt = records per voxel,
   // vcur = chunk cursors of the reordering push (lazy; V entries), vscan =
@@ -188,6 +193,8 @@ void destroy_context(Context* c);
 // Waits for the stream, raises latched device errors as RunAbort.
 void quiesce(Context& c);
 Species& species_at(Context& c, int sid);
+// the host count from the device one (decomposed step), synchronous
+void settle_count(Context& c, Species& s);
 
 // ---- launchers -------------------------------------------------------------
 // ordered: the fast push may keep the store in continuous voxel order (not

@@ -676,14 +676,19 @@ void materialize(Context& c, Species& s) {
 }
 
 void materialize_all(Context& c) {
-  for (auto& s : c.species) materialize(c, s);
+  for (auto& s : c.species) {
+    settle_count(c, s);
+    materialize(c, s);
+  }
 }
 // Order-free reads (charge deposit, energy sums): a species in continuous
 // voxel order is read where it lies (its n records are all valid); only a
 // deferred sort permutation is applied.
 void materialize_for_sums(Context& c) {
-  for (auto& s : c.species)
+  for (auto& s : c.species) {
+    settle_count(c, s);
     if (!s.ordered) materialize(c, s);
+  }
 }
 
 // sort_particles (particles.cpp:412-458).
