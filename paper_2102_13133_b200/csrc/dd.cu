@@ -96,7 +96,7 @@ void NCCL_OK(ncclResult_t r, const char* what) {
 __global__ void dd_pack_kernel(GridC g, const unsigned* __restrict__ idx, const unsigned* __restrict__ cnt,
                                unsigned lcap, float4* __restrict__ pos, const float4* __restrict__ mom,
                                float4* __restrict__ low, float4* __restrict__ high, unsigned bcap,
-                               int* __restrict__ err) {
+                               int* __restrict__ err, unsigned* __restrict__ vcnt) {
   const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= 2 * lcap) return;
   const int side = t >= lcap ? 1 : 0;
@@ -114,6 +114,7 @@ __global__ void dd_pack_kernel(GridC g, const unsigned* __restrict__ idx, const 
   const unsigned rest = fast_div((unsigned)v, g.mag_pnx);
   const int ix = v - (int)rest * g.pnx;
   p.w = __int_as_float(v - ix + (ix == 0 ? g.nx : 1));
+  if (vcnt) atomicAdd(vcnt + v, 0xffffffffu);  // it was counted in its ghost voxel: it leaves
   buf[2 + 2 * (size_t)k] = p;
   buf[3 + 2 * (size_t)k] = mom[i];
   pos[i].w = __int_as_float(-1);  // a hole
@@ -151,7 +152,8 @@ __global__ void dd_fill_kernel(const unsigned* __restrict__ holes, const unsigne
 __global__ void dd_append_kernel(const unsigned* __restrict__ cnt, unsigned lcap,
                                  const unsigned long long* __restrict__ dn, const float4* __restrict__ from_low,
                                  const float4* __restrict__ from_high, unsigned bcap, unsigned long long cap,
-                                 float4* __restrict__ pos, float4* __restrict__ mom, int* __restrict__ err) {
+                                 float4* __restrict__ pos, float4* __restrict__ mom, int* __restrict__ err,
+                                 unsigned* __restrict__ vcnt) {
   const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= 2 * bcap) return;
   const unsigned E = min(cnt[0], lcap) + min(cnt[1], lcap);
@@ -171,8 +173,10 @@ __global__ void dd_append_kernel(const unsigned* __restrict__ cnt, unsigned lcap
     return;
   }
   if (dst >= cap) return;
-  pos[dst] = src[0];
+  const float4 p = src[0];
+  pos[dst] = p;
   mom[dst] = src[1];
+  if (vcnt) atomicAdd(vcnt + __float_as_int(p.w), 1u);  // counted in the voxel it arrives in
 }
 
 // the new count; emigrant counters and list counters cleared
@@ -203,13 +207,24 @@ struct DD {
     float4* buf[4] = {};  // send down, send up, receive from up, receive from down
     unsigned cap = 0;     // records per buffer
     unsigned* lists = nullptr;  // holes [2 lcap], fillers [2 lcap], counters [2]
+    // physical voxel order: pushes since the last reordering one; vcur
+    // ready (the previous step counted); this step's push counted
+    unsigned since = 0;
+    bool counts_ready = false, counted = false;
   };
   std::vector<Mig> mig;
-  // CUDA graph of the step (its NCCL calls included)
-  cudaGraphExec_t exec = nullptr;
-  std::vector<uint64_t> key;
-  int seen = 0;
+  // CUDA graphs of the step (NCCL calls included), one per host state;
+  // replay re-applies the state the capture produced
+  struct Graph {
+    std::vector<uint64_t> key;
+    cudaGraphExec_t exec = nullptr;
+    std::vector<Context::SpeciesState> post;
+    std::vector<Mig> mig_post;
+  };
+  std::vector<Graph> graphs;
+  std::vector<std::vector<uint64_t>> seen;
   bool use_graphs = true;
+  bool order = true;  // physical voxel order (PIC_VOXEL_ORDER=0: in-place pushes + the radix sort)
 
   void exchange(void* const* b, size_t bytes) {
     NcclApi& n = nccl();
@@ -240,6 +255,7 @@ struct DD {
     for (size_t i = 0; i < x.species.size(); ++i) {
       Species& s = x.species[i];
       ensure_mig_lists(x, s);
+      ensure_count_buffers(x, s);
       if (!s.dn) CUDA_OK(cudaMalloc(&s.dn, sizeof(unsigned long long)));
       Mig& m = mig[i];
       if (m.cap) continue;
@@ -261,17 +277,20 @@ struct DD {
       unsigned* fillers = m.lists + 2 * (size_t)lcap;
       unsigned* nlist = m.lists + 4 * (size_t)lcap;
       const unsigned b2 = (2 * lcap + 255) / 256;
+      unsigned* vc = m.counted ? s.vcnt : nullptr;  // keep this step's counts true through the migration
       dd_pack_kernel<<<b2, 256, 0, x.stream>>>(x.gc, s.mig_idx, s.mig_count, lcap, s.pos, s.mom, m.buf[0],
-                                              m.buf[1], m.cap, x.d_err);
+                                              m.buf[1], m.cap, x.d_err, vc);
       dd_lists_kernel<<<b2, 256, 0, x.stream>>>(s.mig_idx, s.mig_count, lcap, s.dn, s.pos, holes, fillers, nlist);
       dd_fill_kernel<<<b2, 256, 0, x.stream>>>(holes, fillers, nlist, 2 * lcap, s.pos, s.mom);
       x.count_launch(3);
       void* b[4] = {m.buf[0], m.buf[1], m.buf[2], m.buf[3]};
       exchange(b, (size_t)(m.cap + 1) * 32);
       dd_append_kernel<<<(2 * m.cap + 255) / 256, 256, 0, x.stream>>>(s.mig_count, lcap, s.dn, m.buf[3], m.buf[2],
-                                                                       m.cap, s.cap, s.pos, s.mom, x.d_err);
+                                                                       m.cap, s.cap, s.pos, s.mom, x.d_err, vc);
       dd_count_kernel<<<1, 1, 0, x.stream>>>(s.mig_count, lcap, s.dn, m.buf[3], m.buf[2], s.cap, nlist);
       x.count_launch(2);
+      if (m.counted) scan_voxel_counts(x, s);  // chunk starts for the next reordering push
+      m.counts_ready = m.counted;
     }
   }
 
@@ -288,7 +307,29 @@ struct DD {
     launch_load_interpolators(x);
     x.phase_end();
     x.phase_begin(Context::kPhPush);
-    for (auto& s : x.species) launch_advance_p(x, s, exact, false);
+    // physical voxel order: every reorder_interval-th push (and the one
+    // after a blocked sort) writes the store in voxel chunks, the one before
+    // it counts the new voxels; the counts follow the migration
+    const unsigned mi = (unsigned)std::max(1, x.reorder_interval);
+    for (size_t i = 0; i < x.species.size(); ++i) {
+      Species& s = x.species[i];
+      Mig& m = mig[i];
+      bool reorder = order && (s.resort_pending || m.since + 1 >= mi);
+      bool count = order && !reorder && m.since + 2 >= mi;
+      if (reorder && !m.counts_ready) {  // the stored voxels' counts, fresh
+        count_stored_voxels(x, s);
+        scan_voxel_counts(x, s);
+      }
+      if (!launch_advance_p_dd(x, s, exact, reorder ? 2 : (count ? 1 : 0))) reorder = count = false;
+      m.counted = reorder || count;
+      if (reorder) {
+        m.since = 0;
+        s.resort_pending = false;
+      } else {
+        ++m.since;
+      }
+      m.counts_ready = false;
+    }
     x.phase_end();
     const int nx = x.gc.nx;
     x.phase_begin(Context::kPhScatter);
@@ -317,12 +358,35 @@ struct DD {
 
 static std::vector<uint64_t> dd_key(const DD& d, unsigned flags) {
   std::vector<uint64_t> k{flags, (uint64_t)(uintptr_t)d.c->stream};
-  for (const auto& s : d.c->species) {
+  for (size_t i = 0; i < d.c->species.size(); ++i) {
+    const Species& s = d.c->species[i];
     k.push_back((uint64_t)(uintptr_t)s.pos);
     k.push_back((uint64_t)(uintptr_t)s.mom);
-    k.push_back(s.perm_pending ? 1u : 0u);
+    k.push_back((s.perm_pending ? 1u : 0u) | (s.resort_pending ? 2u : 0u));
+    if (i < d.mig.size())
+      k.push_back(((uint64_t)d.mig[i].since << 8) | (d.mig[i].counts_ready ? 1u : 0u));
   }
   return k;
+}
+
+static void dd_save(const DD& d, std::vector<Context::SpeciesState>& ss, std::vector<DD::Mig>& ms) {
+  ss.clear();
+  for (const auto& s : d.c->species)
+    ss.push_back({s.pos, s.mom, s.pos_alt, s.mom_alt, s.lidx, s.lidx_alt, s.perm_pending, s.ordered,
+                  s.resort_pending, s.counts_ready, s.since_reorder});
+  ms = d.mig;
+}
+
+static void dd_restore(DD& d, const std::vector<Context::SpeciesState>& ss, const std::vector<DD::Mig>& ms) {
+  for (size_t i = 0; i < ss.size() && i < d.c->species.size(); ++i) {
+    Species& s = d.c->species[i];
+    s.pos = ss[i].pos;
+    s.mom = ss[i].mom;
+    s.pos_alt = ss[i].pos_alt;
+    s.mom_alt = ss[i].mom_alt;
+    s.resort_pending = ss[i].relabel_pending;  // (the slot carries resort_pending here)
+  }
+  d.mig = ms;
 }
 
 void step_graphed_dd(DD& d, unsigned flags) {
@@ -341,14 +405,20 @@ void step_graphed_dd(DD& d, unsigned flags) {
   }
   const bool graphs = d.use_graphs && !c.phase_timing;
   const auto key = dd_key(d, flags);
-  if (graphs && d.exec && d.key == key) {
-    CUDA_OK(cudaGraphLaunch(d.exec, c.stream));
-    ++c.steps_done;
-    return;
-  }
-  if (!graphs || d.key != key || d.seen < 1) {  // plain the first time (allocations, attributes)
-    d.seen = d.key == key ? d.seen + 1 : 1;
-    d.key = key;
+  if (graphs)
+    for (auto& g : d.graphs)
+      if (g.key == key) {
+        CUDA_OK(cudaGraphLaunch(g.exec, c.stream));
+        dd_restore(d, g.post, g.mig_post);
+        ++c.steps_done;
+        return;
+      }
+  if (!graphs || std::find(d.seen.begin(), d.seen.end(), key) == d.seen.end()) {
+    // plain the first time a state comes up (allocations, attributes)
+    if (graphs) {
+      d.seen.push_back(key);
+      if (d.seen.size() > 64) d.seen.erase(d.seen.begin());
+    }
     d.step(flags);
     return;
   }
@@ -362,12 +432,18 @@ void step_graphed_dd(DD& d, unsigned flags) {
     throw;
   }
   CUDA_OK(cudaStreamEndCapture(c.stream, &graph));
-  if (d.exec) cudaGraphExecDestroy(d.exec);
-  d.exec = nullptr;
-  CUDA_OK(cudaGraphInstantiate(&d.exec, graph, 0));
+  DD::Graph g;
+  g.key = key;
+  CUDA_OK(cudaGraphInstantiate(&g.exec, graph, 0));
   CUDA_OK(cudaGraphDestroy(graph));
+  dd_save(d, g.post, g.mig_post);
   --c.steps_done;
-  CUDA_OK(cudaGraphLaunch(d.exec, c.stream));
+  if (d.graphs.size() >= 32) {
+    cudaGraphExecDestroy(d.graphs.front().exec);
+    d.graphs.erase(d.graphs.begin());
+  }
+  d.graphs.push_back(std::move(g));
+  CUDA_OK(cudaGraphLaunch(d.graphs.back().exec, c.stream));
   ++c.steps_done;
 }
 
@@ -405,6 +481,8 @@ int pic_dd_create(pic_context* ctx, int rank, int world, const void* unique_id12
     p->d.high = (rank + 1) % world;
     if (mig_frac > 0) p->d.mig_frac = mig_frac;
     if (const char* v = std::getenv("PIC_DD_GRAPHS")) p->d.use_graphs = std::atoi(v) != 0;
+    p->d.order = c.voxel_order;
+    c.physical_order = p->d.order;
     ncclUniqueId id;
     std::memcpy(&id, unique_id128, sizeof id);
     try {
@@ -435,7 +513,8 @@ int pic_dd_destroy(pic_dd* dd) {
     DD& d = dd->d;
     cudaSetDevice(d.c->device);
     cudaStreamSynchronize(d.c->stream);
-    if (d.exec) cudaGraphExecDestroy(d.exec);
+    for (auto& g : d.graphs) cudaGraphExecDestroy(g.exec);
+    d.c->physical_order = false;
     for (auto& b : d.acc) cudaFree(b);
     for (auto& b : d.fld) cudaFree(b);
     for (auto& m : d.mig) {

@@ -136,7 +136,9 @@ vscan_kernel(unsigned* __restrict__ cnt, unsigned* __restrict__ cur, long long n
 // Particles per stored voxel (the first chunk sizes of a store entering the
 // continuous order): equal voxels of a warp share one atomic.
 __global__ void __launch_bounds__(256)
-voxel_histogram_kernel(const float4* __restrict__ pos, long long n, unsigned* __restrict__ cnt) {
+voxel_histogram_kernel(const float4* __restrict__ pos, long long n, unsigned* __restrict__ cnt,
+                       const unsigned long long* __restrict__ ndev = nullptr) {
+  if (ndev) n = (long long)*ndev;
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int key = i < n ? __float_as_int(__ldcs(pos + i).w) : -1;
   const unsigned peers = __match_any_sync(kFull, key);
@@ -200,6 +202,32 @@ bool voxel_order_usable(const Context& c) {
   return c.voxel_order && !c.gc.xopen && !c.gc.ywall && !c.gc.zwall && !has_walls(c);
 }
 
+void ensure_count_buffers(Context& c, Species& s) {
+  const size_t V = (size_t)c.gc.V;
+  if (!s.vcnt) {
+    const size_t tiles = (V + kScanTile - 1) / kScanTile;
+    CUDA_OK(cudaMalloc(&s.vcnt, V * sizeof(unsigned)));
+    CUDA_OK(cudaMalloc(&s.vcur, V * sizeof(unsigned)));
+    CUDA_OK(cudaMalloc(&s.vscan, (tiles + 1) * sizeof(unsigned)));
+    CUDA_OK(cudaMemsetAsync(s.vcnt, 0, V * sizeof(unsigned), c.stream));
+  }
+  if (!s.pos_alt) {
+    const size_t cap = s.cap ? s.cap : 1;
+    CUDA_OK(cudaMalloc(&s.pos_alt, cap * sizeof(float4)));
+    CUDA_OK(cudaMalloc(&s.mom_alt, cap * sizeof(float4)));
+  }
+}
+
+// records per stored voxel into vcnt (the count may live on the device)
+void count_stored_voxels(Context& c, Species& s) {
+  const long long nl = s.n_on_device ? (long long)s.cap : (long long)s.n;
+  if (nl > 0) {
+    voxel_histogram_kernel<<<blocks_of(nl), 256, 0, c.stream>>>(s.pos, (long long)s.n, s.vcnt,
+                                                                 s.n_on_device ? s.dn : nullptr);
+    c.count_launch();
+  }
+}
+
 static void ensure_order_buffers(Context& c, Species& s) {
   const size_t V = (size_t)c.gc.V;
   const size_t cap = s.cap ? s.cap : 1;
@@ -221,7 +249,7 @@ static void ensure_order_buffers(Context& c, Species& s) {
 }
 
 // vcnt -> vcur (exclusive prefix), vcnt cleared.
-static void scan_voxel_counts(Context& c, Species& s) {
+void scan_voxel_counts(Context& c, Species& s) {
   const long long V = c.gc.V;
   const unsigned tiles = (unsigned)((V + kScanTile - 1) / kScanTile);
   vtile_sum_kernel<<<tiles, kScanThreads, 0, c.stream>>>(s.vcnt, V, s.vscan);

@@ -64,6 +64,7 @@ struct Species {
   // species_ref() settles it back to the host
   unsigned long long* dn = nullptr;
   bool n_on_device = false;
+  bool resort_pending = false;  // physical-order contexts: a blocked sort owed to the next push
   // Voxel order of the fast push's store (order.cu): physical record i is
   // logical (reference-order) record lidx[i]; vcnt = records per voxel,
   // vcur = chunk cursors of the reordering push (lazy; V entries), vscan =
@@ -105,7 +106,10 @@ struct Context {
   int sort_radix_bits = 9;  // LSD digit width (passes = ceil(key bits / width), widths evened out)
   int sort_match = 1;       // group equal digits with match.any (0: per-bit ballots)
   bool sort_defer = true;   // blocked sorts leave the permutation to the next push
-  bool reference_order_sums = false;  // energies in the reference's fp32 order (pic_diagnostics_order)
+  bool reference_order_sums = false;
+  // the decomposed fast step's contexts keep no logical order (particles
+  // migrate between ranks): a blocked sort is a reordering push (dd.cu)
+  bool physical_order = false;  // energies in the reference's fp32 order (pic_diagnostics_order)
   bool voxel_order = true;  // fast periodic pushes keep the store near voxel order (order.cu)
   int reorder_interval = 5;  // every m-th ordered push reorders the store (PIC_REORDER_INTERVAL)
   int num_sms = 148;
@@ -201,6 +205,11 @@ void settle_count(Context& c, Species& s);
 // for chunk views of a species, pic_step_host)
 void launch_advance_p(Context& c, Species& s, bool exact_gyration, bool ordered = true);
 void launch_advance_p_deterministic(Context& c, Species& s, bool exact_gyration);
+// the decomposed step's push (dd.cu): mode 0 in place, 1 in place counting
+// the new voxels, 2 reordering into voxel chunks (physical order only);
+// false: the lean push cannot run (exact_gyration, ranges) and the store
+// was pushed in place without counts
+bool launch_advance_p_dd(Context& c, Species& s, bool exact_gyration, int mode);
 void launch_load_interpolators(Context& c);
 // images: also write B's periodic ghost images (the step's fused ghost sync)
 void launch_advance_b(Context& c, float frac, bool images = false);
@@ -270,6 +279,9 @@ void sort_species(Context& c, Species& s, int order);
 // continuous voxel order (order.cu)
 bool voxel_order_usable(const Context& c);
 void enter_voxel_order(Context& c, Species& s);  // logical indices of the current store
+void ensure_count_buffers(Context& c, Species& s);  // vcnt / vcur / scan, pos_alt (physical order)
+void count_stored_voxels(Context& c, Species& s);   // vcnt += records per stored voxel
+void scan_voxel_counts(Context& c, Species& s);     // vcnt -> vcur, vcnt cleared
 void prepare_reorder(Context& c, Species& s);    // chunk cursors of the stored voxels
 void after_ordered_push(Context& c, Species& s, bool reordered, bool counted);
 void leave_voxel_order(Context& c, Species& s);   // records back into logical order

@@ -693,6 +693,11 @@ void materialize_for_sums(Context& c) {
 
 // sort_particles (particles.cpp:412-458).
 void sort_species(Context& c, Species& s, int order) {
+  if (c.physical_order && !s.ordered && order == PIC_SORT_BLOCKED) {
+    // the decomposed fast path (dd.cu): the next push reorders the store by voxel
+    s.resort_pending = true;
+    return;
+  }
   if (s.ordered && order == PIC_SORT_BLOCKED) {
     // owed to the next push, a reordering one: it groups the store by
     // exactly these voxels, so the stable counting sort becomes a
