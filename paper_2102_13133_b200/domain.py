@@ -178,6 +178,32 @@ class DistTransport:
         return t.cpu().tolist()
 
 
+class HostStagedTransport:
+    """DistTransport over a CPU backend (gloo) for device buffers: every
+    message is staged through host memory (tests of the CUDA engine across
+    processes where NCCL cannot run, e.g. several ranks on one GPU)."""
+
+    def __init__(self, rank: int, world: int, group=None):
+        self.inner = DistTransport(rank, world, group)
+
+    def exchange(self, msgs):
+        staged, back = [], []
+        for src, dst, k, snd, rcv in msgs:
+            hs = snd.cpu() if snd is not None else None
+            hr = None
+            if rcv is not None:
+                hr = rcv.new_empty(rcv.shape, device="cpu")
+                back.append((hr, rcv))
+            staged.append((src, dst, k, hs, hr))
+        self.inner.exchange(staged)
+        for hr, rcv in back:
+            if rcv.numel():
+                rcv.copy_(hr)
+
+    def allreduce(self, values, op="sum"):
+        return self.inner.allreduce(values, op)
+
+
 # ---------------------------------------------------------------------------
 _SLAB_STREAMS = {}
 

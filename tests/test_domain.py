@@ -317,3 +317,65 @@ def test_gloo_world2_global_walls():
         a = gf[lane].reshape(DIMS[2] + 2, DIMS[1] + 2, DIMS[0] + 2)[1:-1, 1:-1, 1:-1]
         b = wf[lane].reshape(DIMS[2] + 2, DIMS[1] + 2, DIMS[0] + 2)[1:-1, 1:-1, 1:-1]
         assert np.abs(a - b).max() <= 1e-4 * max(np.abs(b).max(), 1e-12), lane
+
+
+def _cuda_gloo_worker(rank, world, port, tmp):
+    """One process per slab on the same GPU, the CUDA engine, exchanges over
+    gloo through host memory."""
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle.bindings import Orc
+        from paper_2102_13133_b200.domain import CudaSlab, HostStagedTransport
+        geom = SlabGeometry(16, 6, 5, world=world, dt=0.25)
+        state = _global_state(Orc(), _og(geom.global_grid()), seed=9)
+        slab = CudaSlab(geom.local_grid(), rank, rank == 0, device=0)
+        sim = DecomposedSim(geom, {rank: slab}, HostStagedTransport(rank, world))
+        for si, (q, m, p, ids) in enumerate(state):
+            sid = sim.add_species(f"s{si}", q, m, ids.size)
+            slab.ctx.upload_species(sid, *geom.split(p, ids)[rank])
+        out = {}
+        for k in range(STEPS):
+            sim.step()
+            for si in range(len(SPECIES)):
+                out[f"p{k}_{si}"], out[f"i{k}_{si}"] = slab.ctx.download_species(si)
+            out[f"f{k}"] = slab.ctx.download_fields()
+        d = sim.diagnostics()
+        out["diag"] = np.array([d["e_energy"], d["b_energy"], d["particle_count"]])
+        np.savez(os.path.join(tmp, f"r{rank}.npz"), **out)
+        slab.ctx.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_cuda_engine_world2_gloo_host_staged():
+    """Two processes on one GPU, each with its sm_100a slab, the exchanges
+    over torch.distributed (gloo, host-staged): the global oracle's run."""
+    import socket
+
+    import torch.multiprocessing as mp
+    from oracle.bindings import Orc
+    world = 2
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    with tempfile.TemporaryDirectory() as tmp:
+        mp.spawn(_cuda_gloo_worker, args=(world, port, tmp), nprocs=world, join=True)
+        res = [np.load(os.path.join(tmp, f"r{r}.npz")) for r in range(world)]
+        orc = Orc()
+        geom = SlabGeometry(16, 6, 5, world=world, dt=0.25)
+        og = _og(geom.global_grid())
+        state = _global_state(orc, og, seed=9)
+        f = np.zeros((16, geom.global_grid().padded), np.float32)
+        want = _oracle_run(orc, og, [(q, m, p.copy(), i.copy()) for q, m, p, i in state], f, STEPS)
+        for k in range(STEPS):
+            parts = {r: [(res[r][f"p{k}_{si}"], res[r][f"i{k}_{si}"]) for si in range(len(SPECIES))]
+                     for r in range(world)}
+            _compare(geom, parts, [res[r][f"f{k}"] for r in range(world)], want[k][0], want[k][1], exact=(k == 0))
+        assert np.array_equal(res[0]["diag"], res[1]["diag"])
+        assert res[0]["diag"][2] == sum(ids.size for _, _, _, ids in state)
