@@ -573,6 +573,23 @@ class Context:
         check(fn(self._h, sid, pos.ctypes.data, mom.ctypes.data, lidx.ctypes.data))
         return pos, mom, lidx
 
+    def _push_kernel_ms(self, reset: bool = False):
+        """(cumulative device ms, launches) of the push kernels alone while
+        phase timing is on (events on each launch's own stream)."""
+        fn = lib().pic_internal_push_kernel_ms
+        fn.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_uint64), C.c_int]
+        ms, n = C.c_double(), C.c_uint64()
+        check(fn(self._h, C.byref(ms), C.byref(n), int(reset)))
+        return ms.value, n.value
+
+    def _graph_stats(self):
+        """(captures, replays, plain steps) of pic_step's CUDA graphs."""
+        fn = lib().pic_internal_graph_stats
+        out = (C.c_uint64 * 3)()
+        fn.argtypes = [C.c_void_p, C.c_void_p]
+        check(fn(self._h, out))
+        return tuple(out)
+
     def _set_graphs(self, on: bool):
         """Benchmarking hook (not in the public C header): pic_step as CUDA graphs."""
         fn = lib().pic_internal_set_graphs

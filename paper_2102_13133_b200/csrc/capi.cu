@@ -69,18 +69,46 @@ void Context::phase_end() {
   if (!phase_timing || phase_open < 0) return;
   CUDA_OK(cudaEventRecord(ev_pool[(size_t)ev_marks.back().second + 1], stream));
   phase_open = -1;
-  if (ev_used > 4096) resolve_phases();
+  if (ev_used > 4096 && kev.empty()) resolve_phases();
+}
+
+int Context::kernel_begin() {
+  if (!phase_timing) return -1;
+  if (ev_used + 2 > ev_pool.size()) {
+    for (int k = 0; k < 64; ++k) {
+      cudaEvent_t e;
+      CUDA_OK(cudaEventCreate(&e));
+      ev_pool.push_back(e);
+    }
+  }
+  const int idx = (int)ev_used;
+  CUDA_OK(cudaEventRecord(ev_pool[(size_t)idx], stream));
+  ev_used += 2;
+  return idx;
+}
+
+void Context::kernel_end(int idx) {
+  if (idx < 0) return;
+  CUDA_OK(cudaEventRecord(ev_pool[(size_t)idx + 1], stream));
+  kev.push_back(idx);
 }
 
 void Context::resolve_phases() {
-  if (ev_marks.empty()) return;
-  CUDA_OK(cudaStreamSynchronize(stream));
+  if (ev_marks.empty() && kev.empty()) return;
+  CUDA_OK(cudaDeviceSynchronize());  // push launches may sit on the side streams
   for (const auto& m : ev_marks) {
     float ms = 0;
     CUDA_OK(cudaEventElapsedTime(&ms, ev_pool[(size_t)m.second], ev_pool[(size_t)m.second + 1]));
     phase_ms[m.first] += ms;
   }
+  for (int i : kev) {
+    float ms = 0;
+    CUDA_OK(cudaEventElapsedTime(&ms, ev_pool[(size_t)i], ev_pool[(size_t)i + 1]));
+    push_kernel_ms += ms;
+    ++push_kernel_launches;
+  }
   ev_marks.clear();
+  kev.clear();
   ev_used = 0;
 }
 
@@ -312,7 +340,8 @@ void step(Context& c, unsigned flags) {
   // fast mode without walls: species 1.. on side streams (fork / join; also
   // inside a graph capture), so the small decks' pushes overlap their tails
   const size_t ns = c.species.size();
-  const bool fork = !det && !walls && c.fork_species && ns > 1;
+  // (not while timing phases: each push launch is then timed alone)
+  const bool fork = !det && !walls && c.fork_species && ns > 1 && !c.phase_timing;
   if (fork && !c.side[0]) {
     for (int k = 0; k < Context::kSide; ++k) {
       CUDA_OK(cudaStreamCreateWithFlags(&c.side[k], cudaStreamNonBlocking));
@@ -844,6 +873,7 @@ void step_graphed(Context& c, unsigned flags) {
   for (auto& g : c.graphs) {
     if (g.key == key) {
       CUDA_OK(cudaGraphLaunch(g.exec, c.stream));
+      ++c.graph_replays;
       apply_species_state(c, g.post);
       c.count_launch(g.launches);
       ++c.steps_done;
@@ -853,7 +883,8 @@ void step_graphed(Context& c, unsigned flags) {
   if (std::find(c.graph_seen.begin(), c.graph_seen.end(), key) == c.graph_seen.end()) {
     // first step of a configuration: plain (allocates scratch, sets attributes)
     c.graph_seen.push_back(key);
-    if (c.graph_seen.size() > 32) c.graph_seen.erase(c.graph_seen.begin());
+    if (c.graph_seen.size() > 128) c.graph_seen.erase(c.graph_seen.begin());
+    ++c.graph_plain;
     step(c, flags);
     return;
   }
@@ -873,11 +904,12 @@ void step_graphed(Context& c, unsigned flags) {
   g.key = key;
   g.launches = c.launches - l0;
   g.post = species_state(c);
+  ++c.graph_captures;
   CUDA_OK(cudaGraphInstantiate(&g.exec, graph, 0));
   CUDA_OK(cudaGraphDestroy(graph));
   c.launches = l0;
   c.steps_done = sd;
-  if (c.graphs.size() >= 24) {
+  if (c.graphs.size() >= 64) {
     CUDA_OK(cudaGraphExecDestroy(c.graphs.front().exec));
     c.graphs.erase(c.graphs.begin());
   }
@@ -1173,6 +1205,31 @@ int pic_phase_timings(pic_context* ctx, double out_ms[5], int reset) {
       out_ms[k] = c.phase_ms[k];
       if (reset) c.phase_ms[k] = 0;
     }
+  });
+}
+
+// Not in the public header: cumulative device ms of the push kernels alone
+// and their launch count (phase timing on), the roofline's denominator.
+int pic_internal_push_kernel_ms(pic_context* ctx, double* ms, uint64_t* launches, int reset) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    c.resolve_phases();
+    *ms = c.push_kernel_ms;
+    *launches = c.push_kernel_launches;
+    if (reset) {
+      c.push_kernel_ms = 0;
+      c.push_kernel_launches = 0;
+    }
+  });
+}
+
+// Not in the public header: graph captures / replays / plain steps of pic_step.
+int pic_internal_graph_stats(pic_context* ctx, uint64_t out[3]) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    out[0] = c.graph_captures;
+    out[1] = c.graph_replays;
+    out[2] = c.graph_plain;
   });
 }
 

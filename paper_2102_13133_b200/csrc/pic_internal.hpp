@@ -143,6 +143,7 @@ struct Context {
   };
   std::vector<Graph> graphs;
   std::vector<std::vector<uint64_t>> graph_seen;  // recent keys (captured on their second occurrence)
+  uint64_t graph_captures = 0, graph_replays = 0, graph_plain = 0;
   bool use_graphs = true;
   cudaEvent_t events[64] = {};
   // fast-mode step: species after the first push on side streams (their
@@ -175,6 +176,13 @@ struct Context {
   void phase_begin(int ph);
   void phase_end();
   void resolve_phases();
+  // the push kernels alone (every advance_p launch bracketed by events on
+  // its own stream while phase_timing is on): the roofline's denominator
+  std::vector<int> kev;  // event index of each push launch's start (end = +1)
+  double push_kernel_ms = 0;
+  uint64_t push_kernel_launches = 0;
+  int kernel_begin();
+  void kernel_end(int idx);
 
   // host-buffer step pipeline (pic_step_host): copy-in / copy-out streams,
   // double-buffered staging, ordering events

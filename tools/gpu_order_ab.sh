@@ -6,8 +6,10 @@ out=${1:-gpurun_out/order_ab}
 mkdir -p "$(dirname $out)"
 for cfg in ${CONFIGS:-two_stream thermal weak}; do
   for vo in 1 0; do
-    steps=20; [ $cfg = thermal ] && steps=100
-    PIC_VOXEL_ORDER=$vo python bench.py --config $cfg --steps $steps --warmup 5 --no-cpu-baseline --no-e2e \
+    # thermal (0.35 ms steps): a warm-up of three sort cycles so the step's
+    # CUDA graphs (one per host state of the voxel-order cycle) are captured
+    steps=20; warm=5; [ $cfg = thermal ] && steps=100 && warm=60
+    PIC_VOXEL_ORDER=$vo python bench.py --config $cfg --steps $steps --warmup $warm --no-cpu-baseline --no-e2e \
       > ${out}_${cfg}_vo${vo}.json 2>> ${out}.log
     python - "$cfg" "$vo" "${out}_${cfg}_vo${vo}.json" <<'PY'
 import json, sys
