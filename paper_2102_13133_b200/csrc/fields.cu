@@ -347,6 +347,86 @@ __global__ void fold_z_kernel(GridC g, float* acc) {
   fold_slot(acc, voxel_of(g, ix, iy, g.nz + 1), voxel_of(g, ix, iy, 1));
 }
 
+// The three passes of ghost_fold_currents (grid.cpp:78-99) in one launch
+// for a fully periodic box: each ghost element folds into exactly one
+// interior element (its periodic image, through the x -> y -> z chain), so
+// one thread per interior element on the box's boundary shell gathers its
+// sources with the passes' own additions in their order — the x pass's
+// (A + A[x ghost]), then the y pass's (X + X[y ghost]), then the z pass's
+// (Y + Y[z ghost]) — and zeroes every ghost it read: bit-identical to the
+// sequential passes.
+struct Acc12 {
+  float4 a, b, c;
+};
+__device__ __forceinline__ Acc12 acc_ld(const float4* a, size_t v) { return {a[3 * v], a[3 * v + 1], a[3 * v + 2]}; }
+__device__ __forceinline__ void acc_add(Acc12& t, const Acc12& s) {
+  t.a.x = t.a.x + s.a.x; t.a.y = t.a.y + s.a.y; t.a.z = t.a.z + s.a.z; t.a.w = t.a.w + s.a.w;
+  t.b.x = t.b.x + s.b.x; t.b.y = t.b.y + s.b.y; t.b.z = t.b.z + s.b.z; t.b.w = t.b.w + s.b.w;
+  t.c.x = t.c.x + s.c.x; t.c.y = t.c.y + s.c.y; t.c.z = t.c.z + s.c.z; t.c.w = t.c.w + s.c.w;
+}
+__device__ __forceinline__ void acc_zero(float4* a, size_t v) {
+  a[3 * v] = a[3 * v + 1] = a[3 * v + 2] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
+__global__ void fold_fused_kernel(GridC g, float* acc) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long fx = 2LL * g.ny * g.nz;              // ix = 1, nx
+  const long long fy = 2LL * (g.nx - 2) * g.nz;        // iy = 1, ny (2 <= ix <= nx - 1)
+  const long long fz = 2LL * (g.nx - 2) * (g.ny - 2);  // iz = 1, nz (interior ix, iy)
+  int ix, iy, iz;
+  if (t < fx) {
+    const long long r = t >> 1;
+    ix = (t & 1) ? g.nx : 1;
+    iy = 1 + (int)(r % g.ny);
+    iz = 1 + (int)(r / g.ny);
+  } else if (t < fx + fy) {
+    const long long u = t - fx, r = u >> 1;
+    iy = (u & 1) ? g.ny : 1;
+    ix = 2 + (int)(r % (g.nx - 2));
+    iz = 1 + (int)(r / (g.nx - 2));
+  } else if (t < fx + fy + fz) {
+    const long long u = t - fx - fy, r = u >> 1;
+    iz = (u & 1) ? g.nz : 1;
+    ix = 2 + (int)(r % (g.nx - 2));
+    iy = 2 + (int)(r / (g.nx - 2));
+  } else {
+    return;
+  }
+  float4* a = reinterpret_cast<float4*>(acc);
+  // the x pass's value at (ix, y, z): A + the x ghost that folds onto it
+  auto X = [&](int y, int z) {
+    Acc12 v = acc_ld(a, (size_t)voxel_of(g, ix, y, z));
+    const int gx = ix == g.nx ? 0 : (ix == 1 ? g.nx + 1 : -1);
+    if (gx >= 0) {
+      const size_t s = (size_t)voxel_of(g, gx, y, z);
+      acc_add(v, acc_ld(a, s));
+      acc_zero(a, s);
+    }
+    return v;
+  };
+  // the y pass's value at (ix, iy, z)
+  auto Y = [&](int z) {
+    Acc12 v = X(iy, z);
+    const int gy = iy == g.ny ? 0 : (iy == 1 ? g.ny + 1 : -1);
+    if (gy >= 0) {
+      acc_add(v, X(gy, z));
+      acc_zero(a, (size_t)voxel_of(g, ix, gy, z));
+    }
+    return v;
+  };
+  Acc12 v = Y(iz);
+  const int gz = iz == g.nz ? 0 : (iz == 1 ? g.nz + 1 : -1);
+  if (gz >= 0) {
+    acc_add(v, Y(gz));
+    // the z ghost row at (ix, iy) and the ghosts of its x / y passes
+    acc_zero(a, (size_t)voxel_of(g, ix, iy, gz));
+  }
+  const size_t tv = (size_t)voxel_of(g, ix, iy, iz);
+  a[3 * tv] = v.a;
+  a[3 * tv + 1] = v.b;
+  a[3 * tv + 2] = v.c;
+}
+
 // ---- layout conversion --------------------------------------------------------
 __global__ void pack_species_kernel(const float* __restrict__ l7, const int32_t* __restrict__ ids,
                                     size_t n, float4* __restrict__ pos, float4* __restrict__ mom) {
@@ -500,6 +580,13 @@ void launch_ghost_fold(Context& c) {
   // x -> y -> z; a walled axis folds its mirror images / drops (boundary.cu);
   // x-decomposed: the shared x planes were folded into the neighbours by
   // exchange (a global x wall is folded here)
+  if (!g.xopen && !g.ywall && !g.zwall) {
+    // fully periodic: the three passes in one launch (bit-identical)
+    const long long shell = 2LL * g.ny * g.nz + 2LL * (g.nx - 2) * g.nz + 2LL * (g.nx - 2) * (g.ny - 2);
+    fold_fused_kernel<<<(unsigned)((shell + 255) / 256), 256, 0, c.stream>>>(g, c.acc);
+    c.count_launch();
+    return;
+  }
   if (g.xopen) {
     if (g.wall_p[0] || g.wall_p[1]) launch_wall_fold(c, 0);
   } else {
