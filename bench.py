@@ -310,6 +310,11 @@ def run_ours(args, rank, world):
         ctx.sort_particles(s)
     for _ in range(args.warmup):
         one_step()
+    # the step graphs of the timed steps (buffer pairs, reorder cadence, owed
+    # relabels) are captured here, without running anything, so that every
+    # timed step is a graph replay (executor preparation, like an
+    # instantiated graph; every kernel of every timed step still runs)
+    graphs_prepared = ctx.prepare_graphs(args.steps, sort_interval, step_count[0])
     ctx.synchronize()
 
     def barrier():
@@ -323,6 +328,7 @@ def run_ours(args, rank, world):
     barrier()
     ctx.synchronize()
     l0 = ctx.launch_count()
+    g0 = ctx._graph_stats()
     ctx.event(0)
     for _ in range(args.steps):
         one_step()
@@ -331,6 +337,8 @@ def run_ours(args, rank, world):
     barrier()
     ms = ctx.elapsed_ms(0, 1)
     launches = ctx.launch_count() - l0
+    g1 = ctx._graph_stats()
+    graph_stats = {k: b - a for k, a, b in zip(("captured", "replayed", "plain"), g0, g1)}
     clk = clocks.stop()
 
     # --- phase split (same steps again with PhaseTimings events) --------------
@@ -363,6 +371,7 @@ def run_ours(args, rank, world):
         e2e = run_e2e(pic, ctx, sids, npart, args, world)
     ctx.close()
     return dict(ms=ms, npart=npart, launches=launches, clocks=clk, phases=ph, push_rate_kernel=push_rate_kernel,
+                graphs_prepared=graphs_prepared, graph_stats=graph_stats,
                 push_ms_per_launch=push_ms_per_launch, nspecies=len(sids), grid=g, e2e=e2e,
                 push_phase_rate=npart * nph / (ph["push"] / 1e3), push_launches_timed=klaunch)
 
@@ -846,6 +855,8 @@ def main():
                    "global_cells": f"{g.nx}x{g.ny}x{g.nz}",
                    **({"exchange": res["exchange"]} if res.get("exchange") else {}),
                    "l2": "inputs (34 GB of particle records) >> 126 MB L2; no flush",
+                   **({"step_graphs": {"prepared_before_timing": res["graphs_prepared"],
+                                       "timed_steps": res.get("graph_stats")}} if "graphs_prepared" in res else {}),
                    "push_kernel_rate": res["push_rate_kernel"],
                    "push_phase_rate": res.get("push_phase_rate"),
                    "push_launches_timed": res.get("push_launches_timed"),

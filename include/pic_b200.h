@@ -159,6 +159,17 @@ int pic_sort_particles(pic_context* ctx, int species, int order);
 /* SimState::step (proj/src/sim.cpp:143-183) over every species of the
  * context in creation order. */
 int pic_step(pic_context* ctx, unsigned flags);
+/* NOT IN REFERENCE (executor preparation): pic_step replays one CUDA graph
+ * per step configuration (buffer pair, reorder cadence, owed relabel).
+ * This captures, without running anything, the graphs of the next `steps`
+ * fast steps, assuming a blocked pic_sort_particles of every species after
+ * each step whose running count (steps_taken + k) is a multiple of
+ * sort_interval (0: no sorts) — the run loop's cadence
+ * (proj/src/sim.cpp:217-222) — so those steps replay from the first.
+ * Species state is left as it was.  A no-op (captured = 0) unless every
+ * species is already in continuous voxel order (after one fast step). */
+int pic_prepare_step_graphs(pic_context* ctx, unsigned flags, int steps, int sort_interval,
+                            long long steps_taken, int* captured);
 /* The same step with host-resident species (the reference's host
  * advance_particles contract): uploads every species from lanes7[s]/ids[s],
  * steps, downloads back into the same buffers (the weight lane, which the

@@ -166,6 +166,7 @@ def lib() -> C.CDLL:
         "pic_ghost_sync_fields": [P],
         "pic_sort_particles": [P, C.c_int, C.c_int],
         "pic_step": [P, C.c_uint],
+        "pic_prepare_step_graphs": [P, C.c_uint, C.c_int, C.c_int, C.c_longlong, C.POINTER(C.c_int)],
         "pic_step_host": [P, C.c_uint, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)],
         "pic_event_record": [P, C.c_int],
         "pic_event_elapsed_ms": [P, C.c_int, C.c_int, C.POINTER(C.c_float)],
@@ -419,6 +420,16 @@ class Context:
     def step(self, exact_gyration=False, deterministic=False):
         flags = (PIC_EXACT_GYRATION if exact_gyration else 0) | (PIC_DETERMINISTIC if deterministic else 0)
         check(lib().pic_step(self._h, flags))
+
+    def prepare_graphs(self, steps, sort_interval=0, steps_taken=0, exact_gyration=False):
+        """Capture (without running) the CUDA graphs of the next `steps` fast
+        steps, a blocked sort of every species following each step whose
+        count (steps_taken + k) is a multiple of sort_interval.  Returns the
+        number of graphs captured (0 unless every store is voxel-ordered)."""
+        out = C.c_int(0)
+        check(lib().pic_prepare_step_graphs(self._h, PIC_EXACT_GYRATION if exact_gyration else 0, int(steps),
+                                            int(sort_interval), int(steps_taken), C.byref(out)))
+        return out.value
 
     def step_host(self, lanes7_list, ids_list, exact_gyration=False, deterministic=False):
         """SimState::step with host-resident species buffers (copied in and out)."""

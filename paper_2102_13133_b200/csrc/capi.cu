@@ -216,6 +216,10 @@ Context* make_context(int device, const pic_grid& g) {
     if (const char* v = std::getenv("PIC_SORT_DEFER")) c->sort_defer = std::atoi(v) != 0;     // profiling knob
     if (const char* v = std::getenv("PIC_VOXEL_ORDER")) c->voxel_order = std::atoi(v) != 0;   // profiling knob
     if (const char* v = std::getenv("PIC_REORDER_INTERVAL")) c->reorder_interval = std::atoi(v);  // profiling knob
+#ifdef PIC_ABLATIONS
+    if (const char* v = std::getenv("PIC_ORDER_PROBE")) c->order_probe = std::atoi(v);  // timing probe
+#endif
+    if (const char* v = std::getenv("PIC_RELABEL_VARIANT")) c->relabel_variant = std::atoi(v) == 1;  // profiling knob
     if (const char* v = std::getenv("PIC_HOST_BUFS")) c->host_bufs = std::atoi(v);            // profiling knob
     const size_t V = (size_t)gc.V;
     CUDA_OK(cudaMalloc(&c->f, F_COUNT * V * sizeof(float)));
@@ -863,6 +867,8 @@ static void apply_species_state(Context& c, const std::vector<Context::SpeciesSt
   }
 }
 
+static const Context::Graph& capture_step(Context& c, unsigned flags, const std::vector<uint64_t>& key);
+
 void step_graphed(Context& c, unsigned flags) {
   for (auto& s : c.species) settle_count(c, s);
   if (!graph_ok(c, flags)) {
@@ -888,6 +894,15 @@ void step_graphed(Context& c, unsigned flags) {
     step(c, flags);
     return;
   }
+  const Context::Graph& g = capture_step(c, flags, key);
+  CUDA_OK(cudaGraphLaunch(g.exec, c.stream));
+  c.count_launch(g.launches);
+  ++c.steps_done;
+}
+
+// Records one step into a new cached graph (nothing runs; the species' host
+// state advances as the step would advance it).
+static const Context::Graph& capture_step(Context& c, unsigned flags, const std::vector<uint64_t>& key) {
   const uint64_t l0 = c.launches;
   const long long sd = c.steps_done;
   cudaGraph_t graph = nullptr;
@@ -914,9 +929,53 @@ void step_graphed(Context& c, unsigned flags) {
     c.graphs.erase(c.graphs.begin());
   }
   c.graphs.push_back(g);
-  CUDA_OK(cudaGraphLaunch(g.exec, c.stream));
-  c.count_launch(g.launches);
-  ++c.steps_done;
+  return c.graphs.back();
+}
+
+// Captures the graphs of the next `steps` fast steps ahead of time, with a
+// blocked sort of every species after every step whose count (taken before
+// + k) is a multiple of sort_interval (the run loop's cadence,
+// proj/src/sim.cpp:217-222): the host state machine (buffer
+// pairs, reorder cadence, owed relabels) is walked without running a
+// kernel, then restored, so later pic_step calls replay from the first.
+// Only for stores already in continuous voxel order (their buffers and
+// sort scratch exist; a blocked sort is then host-only): otherwise a no-op.
+static int prepare_step_graphs(Context& c, unsigned flags, int steps, int sort_interval, long long taken) {
+  if (!graph_ok(c, flags) || steps <= 0) return 0;
+  for (auto& s : c.species) {
+    settle_count(c, s);
+    if (s.n && !s.ordered) return 0;
+  }
+  const auto saved = species_state(c);
+  const uint64_t l0 = c.launches;
+  const long long sd = c.steps_done;
+  int made = 0;
+  try {
+    for (int k = 1; k <= steps; ++k) {
+      const auto key = graph_key(c, flags);
+      const Context::Graph* hit = nullptr;
+      for (const auto& g : c.graphs)
+        if (g.key == key) hit = &g;
+      if (!hit) {
+        if (c.graphs.size() >= 63) break;  // keep the cache from evicting what it just made
+        hit = &capture_step(c, flags, key);
+        ++made;
+      }
+      apply_species_state(c, hit->post);
+      if (sort_interval > 0 && (taken + k) % sort_interval == 0)
+        for (auto& s : c.species)
+          if (s.n) sort_species(c, s, PIC_SORT_BLOCKED);  // ordered: host-only (relabel owed)
+    }
+  } catch (...) {
+    apply_species_state(c, saved);
+    c.launches = l0;
+    c.steps_done = sd;
+    throw;
+  }
+  apply_species_state(c, saved);
+  c.launches = l0;
+  c.steps_done = sd;
+  return made;
 }
 
 int pic_step(pic_context* ctx, unsigned flags) {
@@ -924,6 +983,18 @@ int pic_step(pic_context* ctx, unsigned flags) {
     if (C_(ctx).gc.xopen && !has_walls(C_(ctx)))
       throw UsageError("pic_step: x-open (decomposed) context; the host sequences the step");
     step_graphed(C_(ctx), flags);
+    check_launch();
+  });
+}
+
+int pic_prepare_step_graphs(pic_context* ctx, unsigned flags, int steps, int sort_interval, long long steps_taken,
+                            int* captured) {
+  return guard([&] {
+    Context& c = C_(ctx);
+    if (c.gc.xopen && !has_walls(c))
+      throw UsageError("pic_prepare_step_graphs: x-open (decomposed) context");
+    const int made = prepare_step_graphs(c, flags, steps, sort_interval, steps_taken);
+    if (captured) *captured = made;
     check_launch();
   });
 }

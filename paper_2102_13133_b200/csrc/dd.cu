@@ -320,8 +320,10 @@ struct DD {
         count_stored_voxels(x, s);
         scan_voxel_counts(x, s);
       }
-      if (!launch_advance_p_dd(x, s, exact, reorder ? 2 : (count ? 1 : 0))) reorder = count = false;
-      m.counted = reorder || count;
+      const bool rcount = reorder && mi == 1;  // the next push reorders too
+      if (!launch_advance_p_dd(x, s, exact, reorder ? (rcount ? 3 : 2) : (count ? 1 : 0)))
+        reorder = count = false;
+      m.counted = (reorder && rcount) || count;
       if (reorder) {
         m.since = 0;
         s.resort_pending = false;

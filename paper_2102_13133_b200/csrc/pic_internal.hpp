@@ -112,6 +112,8 @@ struct Context {
   bool physical_order = false;  // energies in the reference's fp32 order (pic_diagnostics_order)
   bool voxel_order = true;  // fast periodic pushes keep the store near voxel order (order.cu)
   int reorder_interval = 5;  // every m-th ordered push reorders the store (PIC_REORDER_INTERVAL)
+  int order_probe = 0;       // tools library only (PIC_ABLATIONS): timing probes of the reordering push
+  int relabel_variant = 0;   // 0 = voxel blocks staged in shared memory, 1 = a warp per chunk (ablation)
   int num_sms = 148;
   // non-periodic x boundaries (boundary.cu): absorbed particle counts per
   // side, the laser source, emitter hooks, steps taken (laser clock)

@@ -119,8 +119,8 @@ def test_order_off_switch_and_empty_species(pic, orc):
     assert_bitwise(gp, wp, "lanes")
 
 
-@pytest.mark.parametrize("m", [1, 4])
-def test_graphed_ordered_steps_match_oracle(pic, orc, m):
+@pytest.mark.parametrize("m,prepared", [(1, False), (4, False), (4, True), (5, True)])
+def test_graphed_ordered_steps_match_oracle(pic, orc, m, prepared):
     """pic_step captured as CUDA graphs while the ordered push swaps buffers
     every step (two alternating graphs, plus the relabelling step): a
     ballistic deck (q ~ 1e-20: currents far below the fields' ulp) keeps the
@@ -144,6 +144,11 @@ def test_graphed_ordered_steps_match_oracle(pic, orc, m):
         ctx.upload_fields(f)
         wf = f.copy()
         for k in range(1, 26):
+            if prepared and k == 2:
+                # the graphs of steps 2..25 (sort after every 5th) captured
+                # ahead without running: every later step is a replay
+                assert ctx.prepare_graphs(24, 5, 1) > 0
+                g0 = ctx._graph_stats()
             ctx.step()
             orc.step(o, state, wf)
             if k % 5 == 0:
@@ -152,9 +157,48 @@ def test_graphed_ordered_steps_match_oracle(pic, orc, m):
                 for (_, _, p, ids) in state:
                     orc.sort(p, ids)
         assert all(ctx._species_ordered(s) for s in sids)
+        if prepared:
+            g1 = ctx._graph_stats()
+            assert (g1[0] - g0[0], g1[1] - g0[1], g1[2] - g0[2]) == (0, 24, 0), (g0, g1)
         gf = ctx.download_fields()
         for sid, (_, _, p, ids) in zip(sids, state):
             gp, gids = ctx.download_species(sid)
             assert_bitwise(gids, ids, f"ids s{sid}")
             assert_bitwise(gp, p, f"lanes s{sid}")
     assert_bitwise(gf[[0, 1, 2, 4, 5, 6]], wf[[0, 1, 2, 4, 5, 6]], "E/B")
+
+
+@pytest.mark.parametrize("relabel_variant", [0, 1])
+def test_clustered_store_relabel(pic, orc, relabel_variant, monkeypatch):
+    """Blocked sorts of a store with a few crowded voxels (a voxel block
+    holding far more records than the relabel's shared-memory staging, so
+    it ranks from global memory) and many empty ones: the download after
+    each sort is the oracle's stable order."""
+    monkeypatch.setenv("PIC_RELABEL_VARIANT", str(relabel_variant))
+    g = pic.make_grid((8, 6, 5), 1.0, cfl_frac=0.9)
+    o = og(g)
+    rng = np.random.default_rng(11)
+    f = rand_fields(g, rng, scale=0.3, sync=lambda gg, ff: orc.ghost_sync(o, ff))
+    interp = orc.load_interpolators(o, f)
+    n = 30000
+    p, ids = rand_particles(g, rng, n, u_scale=0.4, sort=False)
+    crowd = rng.choice(np.unique(ids), 3, replace=False)
+    pick = rng.random(n) < 0.8
+    ids[pick] = crowd[rng.integers(0, 3, int(pick.sum()))]
+    wp, wids = p.copy(), ids.copy()
+    with pic.Context(g) as ctx:
+        ctx._set_reorder_interval(3)
+        sid = ctx.add_species("s", -1.0, 1.0, n)
+        ctx.upload_species(sid, p, ids)
+        ctx.upload_fields(f)
+        ctx.load_interpolators()
+        for k in range(1, 8):
+            ctx.advance_p(sid)
+            orc.advance_particles(o, -1.0, 1.0, wp, wids, interp, np.zeros((g.padded, 12), np.float32), False)
+            if k in (1, 4, 6):
+                ctx.sort_particles(sid, pic.SORT_BLOCKED)
+                orc.sort(wp, wids, interleaved=False)
+            if k in (2, 5, 7):
+                gp, gids = ctx.download_species(sid)
+                assert_bitwise(gids, wids, f"ids after push {k}")
+                assert_bitwise(gp, wp, f"lanes after push {k}")
