@@ -436,6 +436,9 @@ def run_ours_decomposed(args, rank, world):
         ctx.sort_particles(s_)
     for _ in range(args.warmup):
         one_step()
+    # the timed steps' graphs (NCCL exchanges included) captured ahead, on
+    # every rank alike, so every timed step is a replay
+    graphs_prepared = dd.prepare_graphs(args.steps, sort_interval, step_count[0])
     ctx.synchronize()
     clocks = ClockSampler(args.device)
     clocks.start()
@@ -476,6 +479,7 @@ def run_ours_decomposed(args, rank, world):
     dd.close()
     ctx.close()
     return dict(ms=ms, npart=npart_total // world, npart_total=npart_total, launches=launches, clocks=clk,
+                graphs_prepared=graphs_prepared,
                 phases=ph, push_rate_kernel=npart_local * args.steps / (kms / 1e3),
                 push_ms_per_launch=push_ms_per_launch, nspecies=len(sids), grid=geom.global_grid(), e2e=e2e,
                 local_grid=g, decomposed=True, exchange="C++ pic_dd over NCCL (graph-captured)",

@@ -355,6 +355,11 @@ typedef struct pic_dd pic_dd;
 int pic_dd_unique_id(void* out128); /* ncclGetUniqueId, 128 bytes, on rank 0 */
 int pic_dd_create(pic_context* ctx, int rank, int world, const void* unique_id128, double mig_frac, pic_dd** out);
 int pic_dd_step(pic_dd* dd, unsigned flags);
+/* pic_prepare_step_graphs for pic_dd_step (same arguments; every rank must
+ * call it with the same values, as every rank captures the same exchange
+ * sequence).  A no-op until one pic_dd_step has run. */
+int pic_dd_prepare_graphs(pic_dd* dd, unsigned flags, int steps, int sort_interval, long long steps_taken,
+                          int* captured);
 int pic_dd_destroy(pic_dd* dd);
 
 /* ---- decks and the SimState run surface ---------------

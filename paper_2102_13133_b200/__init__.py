@@ -662,6 +662,16 @@ class DecomposedStep:
         fn.argtypes = [C.c_void_p, C.c_uint]
         check(fn(self._h, PIC_EXACT_GYRATION if exact_gyration else 0))
 
+    def prepare_graphs(self, steps, sort_interval=0, steps_taken=0, exact_gyration=False):
+        """pic_dd_prepare_graphs: capture the next `steps` decomposed steps'
+        graphs ahead (same call on every rank); returns graphs captured."""
+        fn = lib().pic_dd_prepare_graphs
+        fn.argtypes = [C.c_void_p, C.c_uint, C.c_int, C.c_int, C.c_longlong, C.POINTER(C.c_int)]
+        out = C.c_int(0)
+        check(fn(self._h, PIC_EXACT_GYRATION if exact_gyration else 0, int(steps), int(sort_interval),
+                 int(steps_taken), C.byref(out)))
+        return out.value
+
     def close(self):
         if self._h:
             fn = lib().pic_dd_destroy

@@ -391,6 +391,8 @@ static void dd_restore(DD& d, const std::vector<Context::SpeciesState>& ss, cons
   d.mig = ms;
 }
 
+static const DD::Graph& dd_capture(DD& d, unsigned flags, const std::vector<uint64_t>& key);
+
 void step_graphed_dd(DD& d, unsigned flags) {
   Context& c = *d.c;
   if (c.gc.ywall || c.gc.zwall || has_walls(c))
@@ -424,6 +426,15 @@ void step_graphed_dd(DD& d, unsigned flags) {
     d.step(flags);
     return;
   }
+  CUDA_OK(cudaGraphLaunch(dd_capture(d, flags, key).exec, c.stream));
+  ++c.steps_done;
+}
+
+// Records one decomposed step (its NCCL exchanges included) into a new
+// cached graph without running it; the host state advances as the step's.
+static const DD::Graph& dd_capture(DD& d, unsigned flags, const std::vector<uint64_t>& key) {
+  Context& c = *d.c;
+  const uint64_t l0 = c.launches;
   cudaGraph_t graph = nullptr;
   CUDA_OK(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
   try {
@@ -440,13 +451,56 @@ void step_graphed_dd(DD& d, unsigned flags) {
   CUDA_OK(cudaGraphDestroy(graph));
   dd_save(d, g.post, g.mig_post);
   --c.steps_done;
+  c.launches = l0;
   if (d.graphs.size() >= 32) {
     cudaGraphExecDestroy(d.graphs.front().exec);
     d.graphs.erase(d.graphs.begin());
   }
   d.graphs.push_back(std::move(g));
-  CUDA_OK(cudaGraphLaunch(d.graphs.back().exec, c.stream));
-  ++c.steps_done;
+  return d.graphs.back();
+}
+
+// pic_prepare_step_graphs for the decomposed step: the graphs of the next
+// `steps` steps (a blocked sort of every species after each step whose
+// count steps_taken + k is a multiple of sort_interval: host-only here, the
+// next push reorders) captured ahead without running; host state restored.
+// Every rank walks the same state machine, so the captured exchanges match.
+static int dd_prepare(DD& d, unsigned flags, int steps, int sort_interval, long long taken) {
+  Context& c = *d.c;
+  if (!d.use_graphs || c.phase_timing || steps <= 0 || d.mig.size() != c.species.size()) return 0;
+  for (auto& s : c.species)
+    if (!s.n_on_device || s.perm_pending || s.ordered) return 0;
+  std::vector<Context::SpeciesState> ss0;
+  std::vector<DD::Mig> ms0;
+  dd_save(d, ss0, ms0);
+  const long long sd = c.steps_done;
+  const uint64_t l0 = c.launches;
+  int made = 0;
+  try {
+    for (int k = 1; k <= steps; ++k) {
+      const auto key = dd_key(d, flags);
+      const DD::Graph* hit = nullptr;
+      for (const auto& g : d.graphs)
+        if (g.key == key) hit = &g;
+      if (!hit) {
+        if (d.graphs.size() >= 31) break;
+        hit = &dd_capture(d, flags, key);
+        ++made;
+      }
+      dd_restore(d, hit->post, hit->mig_post);
+      if (sort_interval > 0 && (taken + k) % sort_interval == 0)
+        for (auto& s : c.species) sort_species(c, s, PIC_SORT_BLOCKED);  // physical order: host-only
+    }
+  } catch (...) {
+    dd_restore(d, ss0, ms0);
+    c.steps_done = sd;
+    c.launches = l0;
+    throw;
+  }
+  dd_restore(d, ss0, ms0);
+  c.steps_done = sd;
+  c.launches = l0;
+  return made;
 }
 
 }  // namespace picb
@@ -505,6 +559,17 @@ int pic_dd_step(pic_dd* dd, unsigned flags) {
     if (!dd) throw UsageError("pic_dd_step: null");
     CUDA_OK(cudaSetDevice(dd->d.c->device));
     step_graphed_dd(dd->d, flags);
+    CUDA_OK(cudaGetLastError());
+  });
+}
+
+int pic_dd_prepare_graphs(pic_dd* dd, unsigned flags, int steps, int sort_interval, long long steps_taken,
+                          int* captured) {
+  return capi_guard([&] {
+    if (!dd) throw UsageError("pic_dd_prepare_graphs: null");
+    CUDA_OK(cudaSetDevice(dd->d.c->device));
+    const int made = dd_prepare(dd->d, flags, steps, sort_interval, steps_taken);
+    if (captured) *captured = made;
     CUDA_OK(cudaGetLastError());
   });
 }

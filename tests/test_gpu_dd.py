@@ -44,7 +44,8 @@ def test_dd_world1_matches_global_oracle():
         ctx.close()
 
 
-def test_dd_many_steps_conserve_particles_and_match_python_path():
+@pytest.mark.parametrize("prepared", [False, True])
+def test_dd_many_steps_conserve_particles_and_match_python_path(prepared):
     """Twenty graphed steps with heavy x migration, reordering pushes every
     fifth step and after a sort: every particle kept (the device count and
     the voxel counts through the migration), and the state tracks the
@@ -62,9 +63,11 @@ def test_dd_many_steps_conserve_particles_and_match_python_path():
         slab.ctx.upload_species(sid, *geom.split(p, ids)[0])
     try:
         for k in range(1, 21):
+            if prepared and k == 2:  # graphs of steps 2..20 captured ahead (sorts after 8 and 16)
+                assert dd.prepare_graphs(19, 8, 1) > 0
             dd.step()
             sim.step()
-            if k == 8:  # a blocked sort: a reordering push next (physical voxel order)
+            if k % 8 == 0:  # a blocked sort: a reordering push next (physical voxel order)
                 for s in range(len(SPECIES)):
                     ctx.sort_particles(s)
                     slab.ctx.sort_particles(s)
