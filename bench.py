@@ -207,10 +207,13 @@ def measured_peak_gbs():
         return 6650.0, "fallback"
 
 
-def profile_traffic():
+def profile_traffic(config="two_stream"):
     """DRAM bytes (read + write) per advance_p launch and per push from the
-    committed ncu --set full summary of the default kernel (profiles/)."""
-    path = os.path.join(ROOT, "profiles", "advance_p_ncu.json")
+    committed ncu --set full summary of the default kernel over a reorder
+    cycle (profiles/advance_p_ncu.json for the headline two-stream workload,
+    profiles/advance_p_ncu_<config>.json for the others; None if absent)."""
+    name = "advance_p_ncu.json" if config == "two_stream" else f"advance_p_ncu_{config}.json"
+    path = os.path.join(ROOT, "profiles", name)
     try:
         with open(path) as fh:
             d = json.load(fh)
@@ -823,7 +826,7 @@ def main():
     value = res.get("npart_total", res["npart"] * world) * args.steps / (res["ms"] / 1e3)
     peak, peak_kind = measured_peak_gbs()
     achieved = res["npart"] / res["nspecies"] * BYTES_PER_PUSH / (res["push_ms_per_launch"] / 1e3) / 1e9
-    prof = profile_traffic()
+    prof = None if world > 1 or args.decomposed else profile_traffic(args.config)
     cpu = None
     if not args.no_cpu_baseline and world == 1 and cfg.get("deck"):
         cpu = {"value": None, "note": "the reference cannot express this deck; see --config two_stream"}

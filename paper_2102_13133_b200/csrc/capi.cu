@@ -869,7 +869,7 @@ static void apply_species_state(Context& c, const std::vector<Context::SpeciesSt
 
 static const Context::Graph& capture_step(Context& c, unsigned flags, const std::vector<uint64_t>& key);
 
-void step_graphed(Context& c, unsigned flags) {
+static void step_graphed_impl(Context& c, unsigned flags) {
   for (auto& s : c.species) settle_count(c, s);
   if (!graph_ok(c, flags)) {
     step(c, flags);
@@ -982,7 +982,7 @@ int pic_step(pic_context* ctx, unsigned flags) {
   return guard([&] {
     if (C_(ctx).gc.xopen && !has_walls(C_(ctx)))
       throw UsageError("pic_step: x-open (decomposed) context; the host sequences the step");
-    step_graphed(C_(ctx), flags);
+    step_graphed_impl(C_(ctx), flags);
     check_launch();
   });
 }
@@ -1361,3 +1361,5 @@ int pic_launch_count(pic_context* ctx, uint64_t* out) {
 }
 
 }  // extern "C"
+
+void picb::step_graphed(Context& c, unsigned flags) { step_graphed_impl(c, flags); }

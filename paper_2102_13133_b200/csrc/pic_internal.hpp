@@ -335,6 +335,7 @@ inline void set_push_variant(Context& c, int v) {
 
 // ---- the step --------------------------------------------------------------
 void step(Context& c, unsigned flags);
+void step_graphed(Context& c, unsigned flags);  // pic_step: one CUDA graph per step configuration
 
 // C-ABI error translation (capi.cu): runs fn, maps the exception classes to
 // pic_status codes and records the message for pic_last_error().

@@ -518,8 +518,8 @@ struct Sim {
     launch_compute_div_errors(*ctx);
   }
 
-  void do_step() {  // SimState::step (sim.cpp:143-183)
-    step(*ctx, flags());
+  void do_step() {  // SimState::step (sim.cpp:143-183), replayed as CUDA graphs where it can be
+    step_graphed(*ctx, flags());
     ++step_count;
   }
 

@@ -65,7 +65,13 @@ print("ablations ok")
 """
 
 
-@pytest.mark.skipif(not os.path.exists(ABLATE), reason="libpic_b200_ablate.so not built (build.py --ablate)")
+def _ablate_current():
+    from paper_2102_13133_b200 import build
+    return build.up_to_date(ABLATE)
+
+
+@pytest.mark.skipif(not os.path.exists(ABLATE) or not _ablate_current(),
+                    reason="libpic_b200_ablate.so not built or older than the sources (build.py --ablate)")
 def test_ablation_strategies_in_tools_library():
     env = dict(os.environ, PIC_LIB_PATH=ABLATE)
     r = subprocess.run([sys.executable, "-c", f"ROOT = {ROOT!r}\n" + SCRIPT], cwd=ROOT, env=env,

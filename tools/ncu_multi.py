@@ -13,7 +13,7 @@ out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_outpu
 rows = list(csv.reader(io.StringIO(out)))
 hdr, units = rows[0], rows[1]
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0,
-         "second": 1e3}
+         "second": 1e3, "ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}
 KIND = {"0": "in-place", "1": "counting", "2": "reordering"}
 res = []
 for r in rows[2:]:
