@@ -49,13 +49,18 @@ def up_to_date(out: str = OUT) -> bool:
     return all(os.path.getmtime(p) <= t for p in _deps())
 
 
-def build(verbose: bool = False, force: bool = False, ablate: bool = False) -> str:
+def build(verbose: bool = False, force: bool = False, ablate: bool = False, defines=(), tag: str = "") -> str:
+    """tag + defines: an A/B build (e.g. tag "scalar", defines ["PIC_PACKED=0"])
+    into libpic_b200_<tag>.so, selected at run time by PIC_LIB_PATH."""
     out, bdir = (OUT_ABLATE, BUILD_ABLATE) if ablate else (OUT, BUILD)
+    if tag:
+        out = os.path.join(HERE, f"libpic_b200_{tag}.so")
+        bdir = os.path.join(ROOT, "build", f"pic_b200_{tag}")
     if not force and up_to_date(out):
         return out
     os.makedirs(bdir, exist_ok=True)
     srcs = _sources()
-    extra = ["-DPIC_ABLATIONS"] if ablate else []
+    extra = (["-DPIC_ABLATIONS"] if ablate else []) + ["-D" + d for d in defines]
 
     def compile_one(src):
         obj = os.path.join(bdir, os.path.basename(src) + ".o")
@@ -79,4 +84,8 @@ def build(verbose: bool = False, force: bool = False, ablate: bool = False) -> s
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, ablate="--ablate" in sys.argv))
+    # python build.py [-v] [-f] [--ablate] [--tag NAME -DNAME=VALUE ...]
+    tag = sys.argv[sys.argv.index("--tag") + 1] if "--tag" in sys.argv else ""
+    defs = [a[2:] for a in sys.argv if a.startswith("-D")]
+    print(build(verbose="-v" in sys.argv, force="-f" in sys.argv, ablate="--ablate" in sys.argv,
+                defines=defs, tag=tag))

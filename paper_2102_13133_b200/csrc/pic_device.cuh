@@ -156,6 +156,11 @@ __device__ __forceinline__ void tma_load_1d(void* smem_dst, const void* gmem_src
       : "memory");
 }
 
+// global -> L2 bulk prefetch (no completion; bytes % 16 == 0)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* gmem_src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gmem_src), "r"(bytes) : "memory");
+}
+
 // shared -> global bulk copy (bulk-group completion; bytes % 16 == 0)
 __device__ __forceinline__ void tma_store_1d(void* gmem_dst, const void* smem_src, unsigned bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem_dst),
