@@ -212,6 +212,7 @@ Context* make_context(int device, const pic_grid& g) {
     CUDA_OK(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
     if (const char* v = std::getenv("PIC_PUSH_VARIANT")) set_push_variant(*c, std::atoi(v));  // profiling knob
     if (const char* v = std::getenv("PIC_FORK_SPECIES")) c->fork_species = std::atoi(v) != 0;  // profiling knob
+    if (const char* v = std::getenv("PIC_BATCH_SPECIES")) c->batch_species = std::atoi(v) != 0;  // A/B knob
     if (const char* v = std::getenv("PIC_SORT_VARIANT")) set_sort_variant(*c, std::atoi(v));  // profiling knob
     if (const char* v = std::getenv("PIC_SORT_DEFER")) c->sort_defer = std::atoi(v) != 0;     // profiling knob
     if (const char* v = std::getenv("PIC_VOXEL_ORDER")) c->voxel_order = std::atoi(v) != 0;   // profiling knob
@@ -344,8 +345,10 @@ void step(Context& c, unsigned flags) {
   // fast mode without walls: species 1.. on side streams (fork / join; also
   // inside a graph capture), so the small decks' pushes overlap their tails
   const size_t ns = c.species.size();
+  // every species in one launch per push form where the deck allows it
+  const bool batched = !det && !walls && c.batch_species && launch_advance_p_batch(c, exact);
   // (not while timing phases: each push launch is then timed alone)
-  const bool fork = !det && !walls && c.fork_species && ns > 1 && !c.phase_timing;
+  const bool fork = !batched && !det && !walls && c.fork_species && ns > 1 && !c.phase_timing;
   if (fork && !c.side[0]) {
     for (int k = 0; k < Context::kSide; ++k) {
       CUDA_OK(cudaStreamCreateWithFlags(&c.side[k], cudaStreamNonBlocking));
@@ -356,7 +359,7 @@ void step(Context& c, unsigned flags) {
   const size_t nside = fork ? std::min<size_t>(ns - 1, Context::kSide) : 0;
   if (nside) CUDA_OK(cudaEventRecord(c.fork_ev[0], c.stream));
   for (size_t k = 0; k < nside; ++k) CUDA_OK(cudaStreamWaitEvent(c.side[k], c.fork_ev[0], 0));
-  for (size_t i = 0; i < ns; ++i) {
+  for (size_t i = 0; i < ns && !batched; ++i) {
     Species& s = c.species[i];
     if (det) {
       launch_advance_p_deterministic(c, s, exact);

@@ -153,6 +153,7 @@ struct Context {
   // updated accumulator)
   static constexpr int kSide = 3;
   bool fork_species = true;
+  bool batch_species = true;  // one advance_p launch per push form for all species (push.cu)
   cudaStream_t side[kSide] = {};
   cudaEvent_t fork_ev[kSide] = {}, join_ev[kSide] = {};
 
@@ -214,6 +215,7 @@ void settle_count(Context& c, Species& s);
 // ordered: the fast push may keep the store in continuous voxel order (not
 // for chunk views of a species, pic_step_host)
 void launch_advance_p(Context& c, Species& s, bool exact_gyration, bool ordered = true);
+bool launch_advance_p_batch(Context& c, bool exact_gyration);
 void launch_advance_p_deterministic(Context& c, Species& s, bool exact_gyration);
 // the decomposed step's push (dd.cu): mode 0 in place, 1 in place counting
 // the new voxels, 2 reordering into voxel chunks (physical order only);

@@ -45,12 +45,15 @@ def test_kernels_are_the_cuda_path():
     accumulator, no local-memory traffic; the sort ranks with MATCH."""
     sass = subprocess.run(["cuobjdump", "-sass", LIB], capture_output=True, text=True).stdout
     funcs = re.split(r"\n\s+Function : ", sass)
-    push = [f for f in funcs if f.startswith("_ZN4picb14advance_p_leanILi8ELi6ELb0ELb0ELi0ELi4ELi0ELb0ELb1E")]
+    # the default in-place form: kOrd = 0, packed FP32 (kPk = 1)
+    push = [f for f in funcs
+            if f.startswith("_ZN4picb14advance_p_leanILi8ELi6ELb0ELb0ELi0ELi4ELi0ELb0ELb1ELi0ELb0ELi0ELb1E")]
     assert push, "default advance_p kernel not found"
     body = push[0]
     assert "REDG.E.ADD.F32x4" in body
     assert "UBLKCP" in body  # cp.async.bulk (TMA) slice loads / stores
     assert "LDL" not in body and "STL" not in body  # no spills
+    assert "FFMA2" in body and "FADD2" in body  # packed FP32 push arithmetic
     scatter = [f for f in funcs if "radix_scatter_kernel" in f.split("\n", 1)[0]]
     assert scatter and any("MATCH" in f for f in scatter)
 

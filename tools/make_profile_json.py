@@ -24,7 +24,8 @@ out = {"kernel": label, "workload": workload, "launches": launches, "dram_bytes_
        "dram_bytes_per_launch": per_push * npart, "mean_launch_ms": ms,
        "mean_algorithmic_GBs": npart * 64 / (ms * 1e-3) / 1e9,
        "note": "ncu --set full --clock-control none, consecutive advance_p launches over one reorder cycle "
-               "(in-place x3, counting, reordering per species, cold caches, serialised); per push = "
+               "(in-place x3, counting, reordering; one launch pushes every species of the deck; cold caches, "
+               "serialised); per push = "
                "(dram read + write) / particles, averaged over the cycle"}
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 json.dump(out, open(os.path.join(root, "profiles", out_name), "w"), indent=1)

@@ -25,7 +25,9 @@ for r in rows[2:]:
 
     name = g["Kernel Name"][0]
     targs = name[name.find("<") + 1:name.find(">")].split(",")
-    kind = KIND.get(targs[-1].strip(), "?") if "advance_p_lean" in name else name.split("(")[0]
+    # kOrd is the 12th template argument (a 13th, kPk, follows since round 2)
+    kind = KIND.get(targs[11 if len(targs) > 12 else -1].strip(), "?") if "advance_p_lean" in name \
+        else name.split("(")[0]
     dram = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
     ms = num("gpu__time_duration.sum")
     st = sorted(((h[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")], float(v[0] or 0))

@@ -23,4 +23,4 @@ ts = sum(a[0] for a in recs) or 1
 ti = sum(a[1] for a in recs) or 1
 print(f"total samples {ts:.0f}, warp instructions {ti:.4g}")
 for s, n, a, src in sorted(recs, key=lambda t: -t[0])[:top]:
-    print(f"{s / ts * 100:5.1f}% smp {n / ti * 100:5.1f}% inst {a} {src}")
+    print(f"{s / ts * 100:7.3f}% smp {n / ti * 100:7.3f}% inst {a} {src}")

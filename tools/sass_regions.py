@@ -1,14 +1,18 @@
 """Stall samples of an advance_p_lean launch by kernel region.
 
-python tools/sass_regions.py CUBIN_SASS_GI FUNC_SUBSTR NCU_SASS_TXT [...]
+python tools/sass_regions.py OBJ FUNC_SUBSTR NCU_SASS_TXT [...]
 
-CUBIN_SASS_GI: `nvdisasm -gi` of the library's push cubin (same build as
-profiled); NCU_SASS_TXT: tools/ncu_sass_top.py output with every
+OBJ: build/pic_b200/push.cu.o of the library build that was profiled (it is
+disassembled with `nvdisasm -gi`; the source must be the one it was built
+from); NCU_SASS_TXT: tools/ncu_sass_top.py output with every
 instruction.  Each SASS address is attributed to the outermost push.cu line
 of the kernel body, and lines to regions by the markers below.
 """
+import os
 import re
+import subprocess
 import sys
+import tempfile
 from collections import Counter, defaultdict
 
 gi, func = sys.argv[1], sys.argv[2]
@@ -39,7 +43,10 @@ def region(ln):
     return r
 
 
-text = open(gi).read()
+with tempfile.TemporaryDirectory() as td:
+    subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(gi)], cwd=td, check=True, capture_output=True)
+    cub = [f for f in os.listdir(td) if f.endswith(".cubin")][0]
+    text = subprocess.run(["nvdisasm", "-gi", os.path.join(td, cub)], capture_output=True, text=True).stdout
 start = [m.start() for m in re.finditer(r"^\.text\.(\S+):", text, re.M) if func in text[m.start():m.start() + 400]]
 body = text[start[0]:]
 nxt = re.search(r"^\s*\.section\s+\.text\.", body[10:], re.M)
