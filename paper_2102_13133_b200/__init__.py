@@ -593,6 +593,15 @@ class Context:
         check(fn(self._h, C.byref(ms), C.byref(n), int(reset)))
         return ms.value, n.value
 
+    def _batched_launches(self) -> int:
+        """advance_p launches that pushed several species at once (host
+        count of captured and plain steps)."""
+        fn = lib().pic_internal_batched_launches
+        out = C.c_uint64()
+        fn.argtypes = [C.c_void_p, C.c_void_p]
+        check(fn(self._h, C.byref(out)))
+        return out.value
+
     def _graph_stats(self):
         """(captures, replays, plain steps) of pic_step's CUDA graphs."""
         fn = lib().pic_internal_graph_stats

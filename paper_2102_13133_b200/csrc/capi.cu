@@ -1307,6 +1307,12 @@ int pic_internal_graph_stats(pic_context* ctx, uint64_t out[3]) {
   });
 }
 
+// Not in the public header: advance_p_lean launches that pushed several
+// species at once (host-side count: captures and plain steps, not replays).
+int pic_internal_batched_launches(pic_context* ctx, uint64_t* out) {
+  return guard([&] { *out = C_(ctx).batched_launches; });
+}
+
 // Not in the public header: sort strategy (benchmarking).
 int pic_internal_set_sort_variant(pic_context* ctx, int variant) {
   return guard([&] { set_sort_variant(C_(ctx), variant); });

@@ -154,6 +154,7 @@ struct Context {
   static constexpr int kSide = 3;
   bool fork_species = true;
   bool batch_species = true;  // one advance_p launch per push form for all species (push.cu)
+  uint64_t batched_launches = 0;  // advance_p_lean launches issued for several species at once
   cudaStream_t side[kSide] = {};
   cudaEvent_t fork_ev[kSide] = {}, join_ev[kSide] = {};
 

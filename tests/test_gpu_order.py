@@ -168,6 +168,53 @@ def test_graphed_ordered_steps_match_oracle(pic, orc, m, prepared):
     assert_bitwise(gf[[0, 1, 2, 4, 5, 6]], wf[[0, 1, 2, 4, 5, 6]], "E/B")
 
 
+@pytest.mark.parametrize("nspecies", [3, 4, 5])
+def test_batched_species_mixed_forms_match_oracle(pic, orc, nspecies):
+    """Every species of a fast step in one advance_p_lean launch per push
+    form (launch_advance_p_batch): species sorted at different steps sit at
+    different points of their reorder cycles, so a step mixes in-place,
+    counting and reordering pushes (one launch per form, several species per
+    launch); five species exceed the batch (kMaxBatch 4) and take the
+    per-species path.  Ballistic deck: particles and fields bitwise against
+    the oracle after 23 steps (graph captures and replays included: a
+    configuration seen twice is captured)."""
+    g = pic.make_grid((9, 8, 7), 1.0, cfl_frac=0.9)
+    o = og(g)
+    rng = np.random.default_rng(11)
+    f = rand_fields(g, rng, scale=0.3, sync=lambda gg, ff: orc.ghost_sync(o, ff))
+    species = [(-1e-20, 1.0, 0.5), (1e-20, 4.0, 0.2), (-2e-20, 1.5, 0.4), (1e-20, 9.0, 0.1),
+               (-1e-20, 2.0, 0.3)][:nspecies]
+    sizes = [30000, 17000, 25000, 9000, 12000]
+    state = []
+    with pic.Context(g) as ctx:
+        ctx._set_reorder_interval(4)
+        sids = []
+        for si, (q, m, us) in enumerate(species):
+            p, ids = rand_particles(g, rng, sizes[si], u_scale=us)
+            sid = ctx.add_species(f"s{si}", q, m, sizes[si])
+            ctx.upload_species(sid, p, ids)
+            sids.append(sid)
+            state.append((q, m, p.copy(), ids.copy()))
+        ctx.upload_fields(f)
+        wf = f.copy()
+        # species si sorted after step k when (k + si) % (3 + si) == 0
+        for k in range(1, 24):
+            ctx.step()
+            orc.step(o, state, wf)
+            for si, sid in enumerate(sids):
+                if (k + si) % (3 + si) == 0:
+                    ctx.sort_particles(sid)
+                    orc.sort(state[si][2], state[si][3])
+        batched = ctx._batched_launches()
+        gf = ctx.download_fields()
+        for sid, (_, _, p, ids) in zip(sids, state):
+            gp, gids = ctx.download_species(sid)
+            assert_bitwise(gids, ids, f"ids s{sid}")
+            assert_bitwise(gp, p, f"lanes s{sid}")
+    assert_bitwise(gf[[0, 1, 2, 4, 5, 6]], wf[[0, 1, 2, 4, 5, 6]], "E/B")
+    assert (batched > 0) == (nspecies <= 4), batched
+
+
 @pytest.mark.parametrize("relabel_variant", [0, 1])
 def test_clustered_store_relabel(pic, orc, relabel_variant, monkeypatch):
     """Blocked sorts of a store with a few crowded voxels (a voxel block
