@@ -213,6 +213,7 @@ Context* make_context(int device, const pic_grid& g) {
     if (const char* v = std::getenv("PIC_PUSH_VARIANT")) set_push_variant(*c, std::atoi(v));  // profiling knob
     if (const char* v = std::getenv("PIC_FORK_SPECIES")) c->fork_species = std::atoi(v) != 0;  // profiling knob
     if (const char* v = std::getenv("PIC_BATCH_SPECIES")) c->batch_species = std::atoi(v) != 0;  // A/B knob
+    if (const char* v = std::getenv("PIC_FUSED_PROLOGUE")) c->fused_prologue = std::atoi(v) != 0;  // A/B knob
     if (const char* v = std::getenv("PIC_SORT_VARIANT")) set_sort_variant(*c, std::atoi(v));  // profiling knob
     if (const char* v = std::getenv("PIC_SORT_DEFER")) c->sort_defer = std::atoi(v) != 0;     // profiling knob
     if (const char* v = std::getenv("PIC_VOXEL_ORDER")) c->voxel_order = std::atoi(v) != 0;   // profiling knob
@@ -296,7 +297,17 @@ Species& species_at(Context& c, int sid) {
 // accumulator, so moving the unload past them changes no value.
 // Phases as PhaseTimings: interpolate / push / scatter (clear + fold) /
 // field (B, E with the fused unload, B, three ghost syncs).
+static bool fully_periodic(const Context& c) {
+  return !c.gc.xopen && !c.gc.ywall && !c.gc.zwall && !has_walls(c);
+}
+
 static void step_prologue(Context& c) {
+  if (fully_periodic(c) && c.fused_prologue) {  // the clears beside the interpolators, one launch
+    c.phase_begin(Context::kPhInterp);
+    launch_step_prologue_fused(c);
+    c.phase_end();
+    return;
+  }
   c.phase_begin(Context::kPhScatter);
   launch_clear_accumulator(c);  // scatter_->clear()
   launch_clear_currents(c);     // clear_currents(fields_)

@@ -58,8 +58,20 @@ unsigned interior_blocks(const GridC& g, int threads) {
 // shared memory and leave as contiguous 128-bit stores (a record per thread
 // stored directly is five 16-B stores 80 B apart per warp instruction: the
 // LSU throttled at half the DRAM bandwidth).
+// kClear: the step prologue in one launch — the accumulator (scatter_->clear)
+// and the J lanes (clear_currents) zeroed by a grid-stride sweep beside the
+// interpolators (disjoint data)
+template <bool kClear>
 __global__ void __launch_bounds__(256)
-load_interpolators_kernel(GridC g, Lanes L, float4* __restrict__ out) {
+load_interpolators_kernel(GridC g, Lanes L, float4* __restrict__ out, float4* __restrict__ acc) {
+  if (kClear) {
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (long long i = t0; i < 3 * g.V; i += stride) acc[i] = z4;
+    float* __restrict__ j = L.p[F_JX];
+    for (long long i = t0; i < 3 * g.V; i += stride) j[i] = 0.f;
+  }
   __shared__ float4 buf[256 * kInterpF4];
   __shared__ long long sv[256];
   int ix, iy, iz;
@@ -147,8 +159,7 @@ constexpr int kBVox = 4;
 // (B's ghost images written here; E's ghosts are unchanged since the last
 // sync)
 template <bool kImages>
-__global__ void __launch_bounds__(256)
-advance_b_kernel(GridC g, Lanes L, BCoef k) {
+__device__ __forceinline__ void advance_b_chunk(const GridC& g, const Lanes& L, const BCoef& k, long long base) {
   const size_t sx = 1, sy = (size_t)g.sy, sz = (size_t)g.sz;
   const float* __restrict__ ex = L.p[F_EX];
   const float* __restrict__ ey = L.p[F_EY];
@@ -156,7 +167,6 @@ advance_b_kernel(GridC g, Lanes L, BCoef k) {
   float* __restrict__ bx = L.p[F_BX];
   float* __restrict__ by = L.p[F_BY];
   float* __restrict__ bz = L.p[F_BZ];
-  const long long base = (long long)blockIdx.x * (256 * kBVox) + threadIdx.x;
   size_t v[kBVox];
   bool ok[kBVox];
   float e0[kBVox][3], e1[kBVox][6], b0[kBVox][3];
@@ -190,6 +200,12 @@ advance_b_kernel(GridC g, Lanes L, BCoef k) {
   }
 }
 
+template <bool kImages>
+__global__ void __launch_bounds__(256)
+advance_b_kernel(GridC g, Lanes L, BCoef k) {
+  advance_b_chunk<kImages>(g, L, k, (long long)blockIdx.x * (256 * kBVox) + threadIdx.x);
+}
+
 // ---- unload_currents (gather form) + advance_e --------------------------------
 struct ECoef {
   float c1x, c2x, c1y, c2y, c1z, c2z, c3;
@@ -215,11 +231,11 @@ __device__ __forceinline__ float gather4(float jf, float f, float v00, float v01
   return jf;
 }
 
-template <bool kUnload, bool kAdvanceE, bool kImages = false>
-__global__ void __launch_bounds__(256)
-unload_advance_e_kernel(GridC g, Lanes L, const float* __restrict__ acc, ECoef k) {
+template <bool kUnload, bool kAdvanceE, bool kImages>
+__device__ __forceinline__ void unload_e_voxel(const GridC& g, const Lanes& L, const float* acc, const ECoef& k,
+                                               long long idx) {
   int ix, iy, iz;
-  if (!interior_coords(g, (long long)blockIdx.x * blockDim.x + threadIdx.x, ix, iy, iz)) return;
+  if (!interior_coords(g, idx, ix, iy, iz)) return;
   const size_t v = (size_t)voxel_of(g, ix, iy, iz);
   float jx = L.p[F_JX][v], jy = L.p[F_JY][v], jz = L.p[F_JZ][v];
   if (kUnload) {
@@ -265,6 +281,11 @@ unload_advance_e_kernel(GridC g, Lanes L, const float* __restrict__ acc, ECoef k
     // the step's periodic ghost sync fused in: E's images (B's are current)
     if (kImages) write_ghost_images(g, ix, iy, iz, L.p[F_EX], L.p[F_EY], L.p[F_EZ], nex, ney, nez);
   }
+}
+template <bool kUnload, bool kAdvanceE, bool kImages = false>
+__global__ void __launch_bounds__(256)
+unload_advance_e_kernel(GridC g, Lanes L, const float* __restrict__ acc, ECoef k) {
+  unload_e_voxel<kUnload, kAdvanceE, kImages>(g, L, acc, k, (long long)blockIdx.x * blockDim.x + threadIdx.x);
 }
 
 // ---- ghost_sync_fields (fields.cpp:35-58) -----------------------------------
@@ -368,8 +389,7 @@ __device__ __forceinline__ void acc_zero(float4* a, size_t v) {
   a[3 * v] = a[3 * v + 1] = a[3 * v + 2] = make_float4(0.f, 0.f, 0.f, 0.f);
 }
 
-__global__ void fold_fused_kernel(GridC g, float* acc) {
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+__device__ __forceinline__ void fold_shell_item(const GridC& g, float* acc, long long t) {
   const long long fx = 2LL * g.ny * g.nz;              // ix = 1, nx
   const long long fy = 2LL * (g.nx - 2) * g.nz;        // iy = 1, ny (2 <= ix <= nx - 1)
   const long long fz = 2LL * (g.nx - 2) * (g.ny - 2);  // iz = 1, nz (interior ix, iy)
@@ -425,6 +445,12 @@ __global__ void fold_fused_kernel(GridC g, float* acc) {
   a[3 * tv] = v.a;
   a[3 * tv + 1] = v.b;
   a[3 * tv + 2] = v.c;
+}
+__global__ void fold_fused_kernel(GridC g, float* acc) {
+  fold_shell_item(g, acc, (long long)blockIdx.x * blockDim.x + threadIdx.x);
+}
+__host__ __device__ __forceinline__ long long fold_shell_items(const GridC& g) {
+  return 2LL * g.ny * g.nz + 2LL * (g.nx - 2) * g.nz + 2LL * (g.nx - 2) * (g.ny - 2);
 }
 
 // ---- layout conversion --------------------------------------------------------
@@ -522,7 +548,15 @@ __global__ void load_synthetic_kernel(GridC g, int ppc, float u_th, float dx0, f
 
 // ---- launchers -----------------------------------------------------------------
 void launch_load_interpolators(Context& c) {
-  load_interpolators_kernel<<<interior_blocks(c.gc, 256), 256, 0, c.stream>>>(c.gc, lanes_of(c), c.interp);
+  load_interpolators_kernel<false>
+      <<<interior_blocks(c.gc, 256), 256, 0, c.stream>>>(c.gc, lanes_of(c), c.interp, nullptr);
+  c.count_launch();
+}
+
+// clear_accumulator + clear_currents + load_interpolators in one launch
+void launch_step_prologue_fused(Context& c) {
+  load_interpolators_kernel<true><<<interior_blocks(c.gc, 256), 256, 0, c.stream>>>(
+      c.gc, lanes_of(c), c.interp, reinterpret_cast<float4*>(c.acc));
   c.count_launch();
 }
 
@@ -582,7 +616,7 @@ void launch_ghost_fold(Context& c) {
   // exchange (a global x wall is folded here)
   if (!g.xopen && !g.ywall && !g.zwall) {
     // fully periodic: the three passes in one launch (bit-identical)
-    const long long shell = 2LL * g.ny * g.nz + 2LL * (g.nx - 2) * g.nz + 2LL * (g.nx - 2) * (g.ny - 2);
+    const long long shell = fold_shell_items(g);
     fold_fused_kernel<<<(unsigned)((shell + 255) / 256), 256, 0, c.stream>>>(g, c.acc);
     c.count_launch();
     return;

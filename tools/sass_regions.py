@@ -26,7 +26,7 @@ def line_of(marker, start=0):
     raise KeyError(marker)
 
 
-k0 = line_of("advance_p_lean(float4* __restrict__ pos")
+k0 = line_of("advance_p_lean(const LeanBatch B")
 marks = [("prologue", k0), ("order-reserve", line_of("kOrd & 2: every record's slot", k0)),
          ("seeding", line_of("slot seeding (advance_p_run", k0)), ("loop", line_of("#pragma unroll 1", k0)),
          ("flush", line_of("if (kQuad >= 1)", k0)), ("lidx-load", line_of("the logical indices of the slice", k0)),
