@@ -213,6 +213,7 @@ Context* make_context(int device, const pic_grid& g) {
     if (const char* v = std::getenv("PIC_PUSH_VARIANT")) set_push_variant(*c, std::atoi(v));  // profiling knob
     if (const char* v = std::getenv("PIC_FORK_SPECIES")) c->fork_species = std::atoi(v) != 0;  // profiling knob
     if (const char* v = std::getenv("PIC_BATCH_SPECIES")) c->batch_species = std::atoi(v) != 0;  // A/B knob
+    if (const char* v = std::getenv("PIC_INTERLEAVE_SPECIES")) c->interleave_species = std::atoi(v) != 0;  // A/B
     if (const char* v = std::getenv("PIC_FUSED_PROLOGUE")) c->fused_prologue = std::atoi(v) != 0;  // A/B knob
     if (const char* v = std::getenv("PIC_SORT_VARIANT")) set_sort_variant(*c, std::atoi(v));  // profiling knob
     if (const char* v = std::getenv("PIC_SORT_DEFER")) c->sort_defer = std::atoi(v) != 0;     // profiling knob

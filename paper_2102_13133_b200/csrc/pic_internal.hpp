@@ -154,6 +154,7 @@ struct Context {
   static constexpr int kSide = 3;
   bool fork_species = true;
   bool batch_species = true;  // one advance_p launch per push form for all species (push.cu)
+  bool interleave_species = true;  // batched push: species CTAs round robin (push.cu)
   uint64_t batched_launches = 0;  // advance_p_lean launches issued for several species at once
   // fully periodic step: the accumulator / J clears beside the interpolators
   // in one launch (fields.cu)
