@@ -214,7 +214,7 @@ Context* make_context(int device, const pic_grid& g) {
     if (const char* v = std::getenv("PIC_FORK_SPECIES")) c->fork_species = std::atoi(v) != 0;  // profiling knob
     if (const char* v = std::getenv("PIC_BATCH_SPECIES")) c->batch_species = std::atoi(v) != 0;  // A/B knob
     if (const char* v = std::getenv("PIC_INTERLEAVE_SPECIES")) c->interleave_species = std::atoi(v) != 0;  // A/B
-    if (const char* v = std::getenv("PIC_FUSED_PROLOGUE")) c->fused_prologue = std::atoi(v) != 0;  // A/B knob
+    if (const char* v = std::getenv("PIC_FUSE_FIELDS")) c->fuse_fields = std::atoi(v) != 0;  // A/B knob
     if (const char* v = std::getenv("PIC_SORT_VARIANT")) set_sort_variant(*c, std::atoi(v));  // profiling knob
     if (const char* v = std::getenv("PIC_SORT_DEFER")) c->sort_defer = std::atoi(v) != 0;     // profiling knob
     if (const char* v = std::getenv("PIC_VOXEL_ORDER")) c->voxel_order = std::atoi(v) != 0;   // profiling knob
@@ -303,7 +303,7 @@ static bool fully_periodic(const Context& c) {
 }
 
 static void step_prologue(Context& c) {
-  if (fully_periodic(c) && c.fused_prologue) {  // the clears beside the interpolators, one launch
+  if (fully_periodic(c) && c.fuse_fields) {  // the clears beside the interpolators, one launch
     c.phase_begin(Context::kPhInterp);
     launch_step_prologue_fused(c);
     c.phase_end();
@@ -323,6 +323,16 @@ static void step_prologue(Context& c) {
 // after each B half step, Mur's saved planes, the laser source and the wall
 // E condition around the E update.
 static void step_epilogue(Context& c) {
+  if (fully_periodic(c) && c.fuse_fields && c.gc.nx >= 3 && c.gc.ny >= 3) {
+    // fold + first B half step in one launch, then unload + E, B half step;
+    // ghost syncs fused into the updates
+    c.phase_begin(Context::kPhField);
+    launch_fold_advance_b(c);
+    launch_unload_advance_e(c, true, true, true);
+    launch_advance_b(c, 0.5f, true);
+    c.phase_end();
+    return;
+  }
   c.phase_begin(Context::kPhScatter);
   wall_stage(c, PIC_STAGE_FOLD, 0.f);
   launch_ghost_fold(c);

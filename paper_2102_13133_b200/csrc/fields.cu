@@ -158,7 +158,7 @@ constexpr int kBVox = 4;
 // kImages: the step's periodic ghost sync after this update is fused in
 // (B's ghost images written here; E's ghosts are unchanged since the last
 // sync)
-template <bool kImages>
+template <bool kImages, int kBVox = picb::kBVox>
 __device__ __forceinline__ void advance_b_chunk(const GridC& g, const Lanes& L, const BCoef& k, long long base) {
   const size_t sx = 1, sy = (size_t)g.sy, sz = (size_t)g.sz;
   const float* __restrict__ ex = L.p[F_EX];
@@ -200,10 +200,15 @@ __device__ __forceinline__ void advance_b_chunk(const GridC& g, const Lanes& L, 
   }
 }
 
-template <bool kImages>
+template <bool kImages, int kVox = kBVox>
 __global__ void __launch_bounds__(256)
 advance_b_kernel(GridC g, Lanes L, BCoef k) {
-  advance_b_chunk<kImages>(g, L, k, (long long)blockIdx.x * (256 * kBVox) + threadIdx.x);
+  advance_b_chunk<kImages, kVox>(g, L, k, (long long)blockIdx.x * (256 * kVox) + threadIdx.x);
+}
+// a box small enough that kBVox voxels per thread leave the SMs short of
+// warps (C1: 287 k voxels = 281 CTAs): one voxel per thread
+inline int b_vox_for(const GridC& g) {
+  return (long long)g.nx * g.ny * g.nz <= 148LL * 8 * 256 * kBVox ? 1 : kBVox;
 }
 
 // ---- unload_currents (gather form) + advance_e --------------------------------
@@ -449,6 +454,17 @@ __device__ __forceinline__ void fold_shell_item(const GridC& g, float* acc, long
 __global__ void fold_fused_kernel(GridC g, float* acc) {
   fold_shell_item(g, acc, (long long)blockIdx.x * blockDim.x + threadIdx.x);
 }
+// The periodic fold and the first B half step in one launch: they touch
+// disjoint data (the accumulator; E and B), CTAs [0, nfold) fold, the rest
+// advance B (sim.cpp:173-176 order kept: both precede unload + E).
+template <int kVox>
+__global__ void __launch_bounds__(256)
+fold_advance_b_kernel(GridC g, Lanes L, float* acc, BCoef k, unsigned nfold) {
+  if (blockIdx.x < nfold)
+    fold_shell_item(g, acc, (long long)blockIdx.x * 256 + threadIdx.x);
+  else
+    advance_b_chunk<true, kVox>(g, L, k, (long long)(blockIdx.x - nfold) * (256 * kVox) + threadIdx.x);
+}
 __host__ __device__ __forceinline__ long long fold_shell_items(const GridC& g) {
   return 2LL * g.ny * g.nz + 2LL * (g.nx - 2) * g.nz + 2LL * (g.nx - 2) * (g.ny - 2);
 }
@@ -568,10 +584,34 @@ void launch_advance_b(Context& c, float frac, bool images) {
   k.c1x = -fdt * rhy; k.c2x = fdt * rhz;
   k.c1y = -fdt * rhz; k.c2y = fdt * rhx;
   k.c1z = -fdt * rhx; k.c2z = fdt * rhy;
-  if (images)
-    advance_b_kernel<true><<<interior_blocks(c.gc, 256 * kBVox), 256, 0, c.stream>>>(c.gc, lanes_of(c), k);
+  const bool one = b_vox_for(c.gc) == 1;
+  const unsigned nb = interior_blocks(c.gc, 256 * (one ? 1 : kBVox));
+  if (images && one)
+    advance_b_kernel<true, 1><<<nb, 256, 0, c.stream>>>(c.gc, lanes_of(c), k);
+  else if (images)
+    advance_b_kernel<true><<<nb, 256, 0, c.stream>>>(c.gc, lanes_of(c), k);
+  else if (one)
+    advance_b_kernel<false, 1><<<nb, 256, 0, c.stream>>>(c.gc, lanes_of(c), k);
   else
-    advance_b_kernel<false><<<interior_blocks(c.gc, 256 * kBVox), 256, 0, c.stream>>>(c.gc, lanes_of(c), k);
+    advance_b_kernel<false><<<nb, 256, 0, c.stream>>>(c.gc, lanes_of(c), k);
+  c.count_launch();
+}
+
+// fold + advance_b(1/2) of a fully periodic box in one launch
+void launch_fold_advance_b(Context& c) {
+  const float fdt = 0.5f * c.grid.dt;
+  const float rhx = 1.0f / c.grid.hx, rhy = 1.0f / c.grid.hy, rhz = 1.0f / c.grid.hz;
+  BCoef k;  // as launch_advance_b(c, 0.5f, ...)
+  k.c1x = -fdt * rhy; k.c2x = fdt * rhz;
+  k.c1y = -fdt * rhz; k.c2y = fdt * rhx;
+  k.c1z = -fdt * rhx; k.c2z = fdt * rhy;
+  const unsigned nfold = (unsigned)((fold_shell_items(c.gc) + 255) / 256);
+  if (b_vox_for(c.gc) == 1)
+    fold_advance_b_kernel<1><<<nfold + interior_blocks(c.gc, 256), 256, 0, c.stream>>>(c.gc, lanes_of(c), c.acc,
+                                                                                       k, nfold);
+  else
+    fold_advance_b_kernel<kBVox><<<nfold + interior_blocks(c.gc, 256 * kBVox), 256, 0, c.stream>>>(
+        c.gc, lanes_of(c), c.acc, k, nfold);
   c.count_launch();
 }
 

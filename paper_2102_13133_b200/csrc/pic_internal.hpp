@@ -157,8 +157,9 @@ struct Context {
   bool interleave_species = true;  // batched push: species CTAs round robin (push.cu)
   uint64_t batched_launches = 0;  // advance_p_lean launches issued for several species at once
   // fully periodic step: the accumulator / J clears beside the interpolators
-  // in one launch (fields.cu)
-  bool fused_prologue = true;
+  // in one launch, the fold beside the first B half step in one launch
+  // (fields.cu)
+  bool fuse_fields = true;
   cudaStream_t side[kSide] = {};
   cudaEvent_t fork_ev[kSide] = {}, join_ev[kSide] = {};
 
@@ -235,6 +236,7 @@ void launch_unload_advance_e(Context& c, bool unload, bool advance_e, bool image
 void launch_ghost_sync(Context& c);
 void launch_ghost_fold(Context& c);
 void launch_step_prologue_fused(Context& c);
+void launch_fold_advance_b(Context& c);
 void launch_clear_currents(Context& c);
 void launch_clear_accumulator(Context& c);
 void launch_pack_species(Context& c, Species& s, const float* lanes7_dev, const int32_t* ids_dev,
