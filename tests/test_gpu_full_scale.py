@@ -122,6 +122,47 @@ def test_full_scale_push_sample_bitwise(c2):
         assert moved > 0.01, f"{name}: the sample should hold face crossers ({moved})"
 
 
+def test_full_scale_step_sample_bitwise(c2):
+    """The step's own push — every species in one interleaved advance_p_lean
+    launch, whichever push form (in place / counting / reordering) the
+    cadence gives — on a 2^20-particle sample per species: the oracle's push
+    of the same records through the interpolators of the step's fields."""
+    import torch
+    from oracle.bindings import Grid as OGrid
+    from oracle.bindings import Orc
+    pic, ctx, g, cfg, sids = c2
+    orc = Orc()
+    og = OGrid(g.nx, g.ny, g.nz, g.hx, g.hy, g.hz, g.dt)
+    rng = np.random.default_rng(9)
+    b0, r0 = ctx._batched_launches(), ctx._graph_stats()[1]
+    for k in range(3):  # three consecutive steps of the reorder cadence
+        f = ctx.download_fields()
+        i18 = orc.load_interpolators(og, f)
+        del f
+        before = []
+        for sid in sids:
+            pos, mom = _records(ctx, sid)
+            idx = torch.from_numpy(np.sort(rng.choice(pos.shape[0], 1 << 20, replace=False))).cuda()
+            before.append((idx, pos[idx].cpu().numpy(), mom[idx].cpu().numpy()))
+            del pos, mom
+        torch.cuda.empty_cache()
+        ctx.step()
+        for sid, (name, q, m, *_rest), (idx, p0, u0) in zip(sids, cfg["species"], before):
+            pos, mom = _records(ctx, sid)
+            p1, u1 = pos[idx].cpu().numpy(), mom[idx].cpu().numpy()
+            del pos, mom
+            torch.cuda.empty_cache()
+            p7 = np.ascontiguousarray(np.concatenate([p0[:, 0:3].T, u0[:, 0:4].T]), np.float32)
+            ids = np.ascontiguousarray(p0[:, 3].view(np.int32))
+            acc = np.zeros((g.padded, 12), np.float32)
+            orc.advance_particles(og, q, m, p7, ids, i18, acc)
+            got = np.concatenate([p1[:, 0:3].T, u1[:, 0:4].T])
+            assert (p1[:, 3].view(np.int32) == ids).all(), f"{name} step {k}: voxel ids"
+            assert (got.view(np.uint32) == p7.view(np.uint32)).all(), f"{name} step {k}: particle lanes"
+    # every step pushed both species in one launch (issued, or replayed from a graph of such a step)
+    assert (ctx._batched_launches() - b0) + (ctx._graph_stats()[1] - r0) >= 3
+
+
 def test_full_scale_gauss_residual(c2):
     pic, ctx, g, cfg, sids = c2
     ctx.refresh_charge_diagnostics()
