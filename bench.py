@@ -373,9 +373,13 @@ def run_ours(args, rank, world):
     if not args.no_e2e and getattr(deck, "laser_ix", None) is None:  # walled decks: no pic_step_host
         e2e = run_e2e(pic, ctx, sids, npart, args, world)
     ctx.close()
+    # --- e2e through the reference's own run surface, state device-resident --
+    e2e_res = None
+    if not args.no_e2e and not cfg.get("deck") and cfg["n"] <= 64 and world == 1:
+        e2e_res = run_e2e_simstate(cfg, args)
     return dict(ms=ms, npart=npart, launches=launches, clocks=clk, phases=ph, push_rate_kernel=push_rate_kernel,
                 graphs_prepared=graphs_prepared, graph_stats=graph_stats,
-                push_ms_per_launch=push_ms_per_launch, nspecies=len(sids), grid=g, e2e=e2e,
+                push_ms_per_launch=push_ms_per_launch, nspecies=len(sids), grid=g, e2e=e2e, e2e_resident=e2e_res,
                 # a launch pushes every species of the deck at once where it
                 # can (one grid per push form): particles per timed launch
                 particles_per_launch=npart * nph / max(klaunch, 1),
@@ -705,6 +709,39 @@ def run_e2e_decomposed(pic, sim, ctx, sids, args, world):
             "note": "per rank: records H2D, decomposed step, records D2H (not pipelined); bytes are rank 0's"}
 
 
+def run_e2e_simstate(cfg, args, steps=None, diag_interval=10):
+    """The reference's own host surface with the state resident on the GPU:
+    the deck text (proj/src/deck.cpp grammar), SimState::initialize (the
+    reference's mt19937_64 load on the host, bit-identical, then uploaded)
+    and SimState::run (sim.cpp:285-306: step, the due sorts, the
+    diagnostics row every diag_interval steps with its charge refresh,
+    written as the reference's CSV).  Timed by the wall clock around a
+    second run() (the first, a warm-up, captures the step graphs of a sort
+    cycle); per step the host reads back only the diagnostics (pic_diag +
+    kinetic per species, every diag_interval steps)."""
+    import tempfile
+
+    from paper_2102_13133_b200.simstate import Deck, SimState
+    steps = steps or cfg["sort_interval"]
+    text = deck_text(cfg).replace("steps = 0", f"steps = {steps}") + f"diag_interval = {diag_interval}\n"
+    sim = SimState.initialize(Deck(text), device=args.device)
+    npart = sum(sim.context.species_count(k) for k in range(len(cfg["species"])))
+    with tempfile.NamedTemporaryFile(suffix=".csv") as f:
+        sim.run(f.name)  # warm-up run: captures the step graphs of a sort cycle (steps = sort_interval)
+        sim.context.synchronize()
+        t0 = time.perf_counter()
+        sim.run(f.name)  # steps more steps, CSV rows on the diag cadence; quiesces at the end
+        dt = time.perf_counter() - t0
+        rows = sum(1 for _ in open(f.name)) - 1
+    sim.close()
+    d2h = (28 + 4 * len(cfg["species"])) * (steps // diag_interval + 1)
+    return {"value": npart * steps / dt, "unit": "particle pushes/s", "h2d_bytes_per_step": 0,
+            "d2h_bytes_per_step": d2h / steps, "steps": steps, "ms_per_step": dt / steps * 1e3,
+            "csv_rows": rows,
+            "path": "pic_sim_run (SimState::run over the deck text; state device-resident, diagnostics "
+                    f"every {diag_interval} steps)"}
+
+
 def run_e2e(pic, ctx, sids, npart, args, world):
     """pic_step_host: every step uploads all species from pinned host
     buffers, steps, and downloads them back (32 B/particle each way)."""
@@ -887,6 +924,7 @@ def main():
                      "bytes_per_push": BYTES_PER_PUSH, "peak_kind": peak_kind},
         "cpu_baseline": cpu,
         "e2e": res["e2e"],
+        **({"e2e_resident": res["e2e_resident"]} if res.get("e2e_resident") else {}),
         "gpu_launches": res["launches"],
         "clocks": res["clocks"],
     }

@@ -965,7 +965,7 @@ static const Context::Graph& capture_step(Context& c, unsigned flags, const std:
 // kernel, then restored, so later pic_step calls replay from the first.
 // Only for stores already in continuous voxel order (their buffers and
 // sort scratch exist; a blocked sort is then host-only): otherwise a no-op.
-static int prepare_step_graphs(Context& c, unsigned flags, int steps, int sort_interval, long long taken) {
+static int prepare_step_graphs_impl(Context& c, unsigned flags, int steps, int sort_interval, long long taken) {
   if (!graph_ok(c, flags) || steps <= 0) return 0;
   for (auto& s : c.species) {
     settle_count(c, s);
@@ -1018,7 +1018,7 @@ int pic_prepare_step_graphs(pic_context* ctx, unsigned flags, int steps, int sor
     Context& c = C_(ctx);
     if (c.gc.xopen && !has_walls(c))
       throw UsageError("pic_prepare_step_graphs: x-open (decomposed) context");
-    const int made = prepare_step_graphs(c, flags, steps, sort_interval, steps_taken);
+    const int made = prepare_step_graphs_impl(c, flags, steps, sort_interval, steps_taken);
     if (captured) *captured = made;
     check_launch();
   });
@@ -1394,3 +1394,6 @@ int pic_launch_count(pic_context* ctx, uint64_t* out) {
 }  // extern "C"
 
 void picb::step_graphed(Context& c, unsigned flags) { step_graphed_impl(c, flags); }
+int picb::prepare_step_graphs(Context& c, unsigned flags, int steps, int sort_interval, long long taken) {
+  return prepare_step_graphs_impl(c, flags, steps, sort_interval, taken);
+}

@@ -141,19 +141,36 @@ div_errors_kernel(GridC g, float* __restrict__ f, float rhx, float rhy, float rh
 }
 
 // deposit_rho (particles.cpp:384-410): eight trilinear weights per particle
-// into the rhof lane.  Same-voxel lanes of a warp (the common case on a
-// voxel-sorted store) are summed with shuffles first; the adds into rhof
-// are float atomics (order not fixed: tolerance parity).
+// into the rhof lane (float atomics, order not fixed: tolerance parity).
+// A CTA's 256 particles of a voxel-ordered store lie in a few consecutive
+// voxels v (plus the ones that moved since the last reorder), whose eight
+// nodes v + {0, 1} + {0, sy} + {0, sz} fall in four short windows of node
+// indices: the CTA adds its contributions there with shared-memory atomics
+// and then adds each window node once into rhof.  Nodes outside the windows
+// (particles moved in y / z, periodic wraps) go straight to global memory.
+// Runs of equal voxels across a warp's lanes are summed with a shuffle scan
+// first, so a sorted warp adds once per node.  Was one global atomic per
+// particle and node in mixed warps (contended on a few nodes): 0.69 ms per
+// 8.4 M particles of an aged store, 0.07 ms sorted.
+constexpr int kRhoWin = 96;  // window nodes from the CTA's base voxel
 __global__ void __launch_bounds__(256)
 deposit_rho_kernel(GridC g, const float4* __restrict__ pos, const float4* __restrict__ mom, long long n,
                    float q, float scale, float* __restrict__ rho) {
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ float win[4][kRhoWin];
+  __shared__ int s_base;
+  const long long i0 = (long long)blockIdx.x * blockDim.x;
+  const long long i = i0 + threadIdx.x;
+  for (int t = threadIdx.x; t < 4 * kRhoWin; t += blockDim.x) (&win[0][0])[t] = 0.f;
+  // the window base: the CTA's first voxel, less a margin for x movers
+  if (threadIdx.x == 0) s_base = __float_as_int(pos[i0].w) - 8;
+  __syncthreads();
+  const int base = s_base;
+  const int off[4] = {0, g.sy, g.sz, g.sy + g.sz};
   const int lane = threadIdx.x & 31;
-  int key = -1;
+  int key = -1, ix = 0, iy = 0, iz = 0;
   float w[8];
 #pragma unroll
   for (int k = 0; k < 8; ++k) w[k] = 0.f;
-  int ix = 0, iy = 0, iz = 0;
   if (i < n) {
     const float4 p = pos[i];
     const float4 u = mom[i];
@@ -176,30 +193,42 @@ deposit_rho_kernel(GridC g, const float4* __restrict__ pos, const float4* __rest
     w[6] = qw * (wxl * wyh * wzh);
     w[7] = qw * (wxh * wyh * wzh);
   }
-  // a warp that holds one voxel (the common case on a sorted store) sums its
-  // eight weights with a butterfly and lane 0 adds them; mixed warps add
-  // per particle.
-  const unsigned peers = __match_any_sync(kFull, key);
-  if (peers == kFull) {
+  // runs of equal voxels across the warp's lanes are first summed with a
+  // segmented shuffle scan: each run's last lane adds its eight sums
+  const int prev = __shfl_up_sync(0xffffffffu, key, 1);
+  const unsigned heads = __ballot_sync(0xffffffffu, lane == 0 || key != prev);
+  const int start = 31 - __clz(heads & (0xffffffffu >> (31 - lane)));
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
+  for (int o = 1; o < 32; o <<= 1) {
 #pragma unroll
-      for (int k = 0; k < 8; ++k) w[k] += __shfl_xor_sync(kFull, w[k], o);
-    if (lane != 0) return;
+    for (int k = 0; k < 8; ++k) {
+      const float y = __shfl_up_sync(0xffffffffu, w[k], o);
+      if (lane - o >= start) w[k] += y;
+    }
   }
-  if (key < 0) return;
-  const float* s = w;
-  const int xh = (ix + 1 > g.nx && !g.xopen) ? 1 : ix + 1;  // x-decomposed: ghost, halo-added
-  const int yh = (iy + 1 > g.ny && !g.ywall) ? 1 : iy + 1;  // walled: the wall node plane
-  const int zh = (iz + 1 > g.nz && !g.zwall) ? 1 : iz + 1;
-  atomicAdd(rho + voxel_of(g, ix, iy, iz), s[0]);
-  atomicAdd(rho + voxel_of(g, xh, iy, iz), s[1]);
-  atomicAdd(rho + voxel_of(g, ix, yh, iz), s[2]);
-  atomicAdd(rho + voxel_of(g, xh, yh, iz), s[3]);
-  atomicAdd(rho + voxel_of(g, ix, iy, zh), s[4]);
-  atomicAdd(rho + voxel_of(g, xh, iy, zh), s[5]);
-  atomicAdd(rho + voxel_of(g, ix, yh, zh), s[6]);
-  atomicAdd(rho + voxel_of(g, xh, yh, zh), s[7]);
+  const bool tail = lane == 31 || ((heads >> (lane + 1)) & 1u);
+  if (tail && key >= 0) {
+    const int xh = (ix + 1 > g.nx && !g.xopen) ? 1 : ix + 1;  // x-decomposed: ghost, halo-added
+    const int yh = (iy + 1 > g.ny && !g.ywall) ? 1 : iy + 1;  // walled: the wall node plane
+    const int zh = (iz + 1 > g.nz && !g.zwall) ? 1 : iz + 1;
+    const int node[8] = {voxel_of(g, ix, iy, iz), voxel_of(g, xh, iy, iz), voxel_of(g, ix, yh, iz),
+                         voxel_of(g, xh, yh, iz), voxel_of(g, ix, iy, zh), voxel_of(g, xh, iy, zh),
+                         voxel_of(g, ix, yh, zh), voxel_of(g, xh, yh, zh)};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int d = node[k] - base - off[k >> 1];  // nodes k = 2j, 2j+1 share window j's offset
+      if (d >= 0 && d < kRhoWin)
+        atomicAdd(&win[k >> 1][d], w[k]);
+      else
+        atomicAdd(rho + node[k], w[k]);
+    }
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < 4 * kRhoWin; t += blockDim.x) {
+    const float v = (&win[0][0])[t];
+    const int j = t / kRhoWin, d = t - j * kRhoWin;
+    if (v != 0.f) atomicAdd(rho + base + off[j] + d, v);
+  }
 }
 
 // kinetic_energy_centered (particles.cpp:468-501): momentum recentred by a

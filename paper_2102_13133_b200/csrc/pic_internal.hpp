@@ -346,6 +346,9 @@ inline void set_push_variant(Context& c, int v) {
 // ---- the step --------------------------------------------------------------
 void step(Context& c, unsigned flags);
 void step_graphed(Context& c, unsigned flags);  // pic_step: one CUDA graph per step configuration
+// the graphs of the next `steps` steps (a blocked sort of every species after
+// each sort_interval-th) captured ahead without running; returns the count
+int prepare_step_graphs(Context& c, unsigned flags, int steps, int sort_interval, long long taken);
 
 // C-ABI error translation (capi.cu): runs fn, maps the exception classes to
 // pic_status codes and records the message for pic_last_error().

@@ -648,6 +648,16 @@ struct Sim {
     namespace fs = std::filesystem;
     if (deck.field_dump_interval > 0) fs::create_directories(deck.out_dir);
     if (csv) *csv << diagnostics_row();
+    // every species sorted (blocked) on one cadence: the graphs of the run's
+    // steps captured ahead (pic_prepare_step_graphs), so every step replays
+    long si = -1;
+    bool one_cadence = !deck.deterministic && !deck.species.empty();
+    for (const auto& ds : deck.species) {
+      if (si < 0) si = ds.sort_interval;
+      one_cadence = one_cadence && ds.sort_interval == si && ds.sort_order == PIC_SORT_BLOCKED;
+    }
+    if (one_cadence && si > 0 && deck.steps > 2)
+      prepare_step_graphs(*ctx, flags(), (int)std::min<long>(deck.steps, 1 << 16), (int)si, step_count);
     for (long i = 0; i < deck.steps; ++i) {
       do_step();
       sort_due();
