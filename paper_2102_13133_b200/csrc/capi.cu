@@ -1242,22 +1242,19 @@ int pic_diagnostics(pic_context* ctx, pic_diag* out, float* kinetic, size_t kine
     if (kinetic_cap < c.species.size() || (!kinetic && !c.species.empty()))
       throw UsageError("diagnostics: kinetic[] smaller than the species count");
     quiesce(c);
-    float eb[2];
-    field_energy(c, eb);
+    float eb[2], mdiv[2];
+    diagnostics_batch(c, eb, kinetic, mdiv);
     out->e_energy = eb[0];
     out->b_energy = eb[1];
     float total = eb[0] + eb[1];
-    launch_load_interpolators(c);  // fresh coefficients (sim.cpp:245-246)
     uint64_t count = 0;
     for (size_t i = 0; i < c.species.size(); ++i) {
-      const float k = kinetic_energy(c, c.species[i], true);
-      kinetic[i] = k;
-      total += k;
+      total += kinetic[i];
       count += c.species[i].n;
     }
     out->total_energy = total;
-    out->max_div_e_err = max_abs_lane(c, F_DIVE);
-    out->max_div_b_err = max_abs_lane(c, F_DIVB);
+    out->max_div_e_err = mdiv[0];
+    out->max_div_b_err = mdiv[1];
     out->particle_count = count;
   });
 }

@@ -512,4 +512,54 @@ float kinetic_energy(Context& c, Species& s, bool centered) {
   return (float)h;
 }
 
+// SimState::current_diagnostics' reductions (sim.cpp:236-266) with one
+// readback: field energy, centred kinetic energy per species (with fresh
+// interpolators) and the two max div errors launched back to back into
+// device slots, one copy, one synchronisation (the synchronous functions
+// above cost a round trip each: 0.58 ms a row at C1).  The fp32 results are
+// those of field_energy / kinetic_energy / max_abs_lane in fast mode; the
+// reference-order sums (deterministic decks) take those functions instead.
+void diagnostics_batch(Context& c, float e_b[2], float* kinetic, float mdiv[2]) {
+  const size_t ns = c.species.size();
+  if (c.reference_order_sums || ns > 24) {
+    field_energy(c, e_b);
+    launch_load_interpolators(c);
+    for (size_t i = 0; i < ns; ++i) kinetic[i] = kinetic_energy(c, c.species[i], true);
+    mdiv[0] = max_abs_lane(c, F_DIVE);
+    mdiv[1] = max_abs_lane(c, F_DIVB);
+    return;
+  }
+  // slots: [0, 2) field energy, [2, 4) max |div e|, |div b| (as u32), [8, 8 + ns) kinetic
+  double* d = reinterpret_cast<double*>(c.scratch_bytes(Context::kScrDiag, 64 * sizeof(double)));
+  CUDA_OK(cudaMemsetAsync(d, 0, (8 + ns) * sizeof(double), c.stream));
+  const long long n = (long long)c.gc.nx * c.gc.ny * c.gc.nz;
+  field_energy_kernel<<<grid_stride_blocks(c, n), 256, 0, c.stream>>>(c.gc, c.f, d);
+  unsigned* mx = reinterpret_cast<unsigned*>(d + 2);
+  max_abs_kernel<<<grid_stride_blocks(c, n), 256, 0, c.stream>>>(c.gc, c.f + (size_t)F_DIVE * c.gc.V, mx);
+  max_abs_kernel<<<grid_stride_blocks(c, n), 256, 0, c.stream>>>(c.gc, c.f + (size_t)F_DIVB * c.gc.V,
+                                                               reinterpret_cast<unsigned*>(d + 3));
+  launch_load_interpolators(c);  // fresh coefficients (sim.cpp:245-246)
+  c.count_launch(3);
+  for (size_t i = 0; i < ns; ++i) {
+    Species& s = c.species[i];
+    if (s.n == 0) continue;
+    const float qdt_2m = (s.q * c.grid.dt) / (2.0f * s.m);
+    kinetic_kernel<true><<<grid_stride_blocks(c, (long long)s.n), 256, 0, c.stream>>>(
+        s.pos, s.mom, (long long)s.n, c.interp, qdt_2m, s.m, d + 8 + i);
+    c.count_launch();
+  }
+  double h[8 + 24];
+  CUDA_OK(cudaMemcpyAsync(h, d, (8 + ns) * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+  CUDA_OK(cudaStreamSynchronize(c.stream));
+  const double hv = 0.5 * (double)((c.grid.hx * c.grid.hy) * c.grid.hz);
+  e_b[0] = (float)(hv * h[0]);
+  e_b[1] = (float)(hv * h[1]);
+  unsigned u[2];
+  std::memcpy(u, &h[2], sizeof(unsigned));
+  std::memcpy(u + 1, &h[3], sizeof(unsigned));
+  std::memcpy(&mdiv[0], &u[0], sizeof(float));
+  std::memcpy(&mdiv[1], &u[1], sizeof(float));
+  for (size_t i = 0; i < ns; ++i) kinetic[i] = c.species[i].n ? (float)h[8 + i] : 0.0f;
+}
+
 }  // namespace picb

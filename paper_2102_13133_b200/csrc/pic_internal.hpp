@@ -284,6 +284,9 @@ void launch_compute_div_errors(Context& c);
 void field_energy(Context& c, float e_b[2]);  // synchronous
 float max_abs_lane(Context& c, int lane);     // synchronous
 float kinetic_energy(Context& c, Species& s, bool centered);  // synchronous
+// current_diagnostics' reductions with one readback (fast mode; the
+// reference-order sums otherwise): e_b, kinetic[species], max |div e|, |div b|
+void diagnostics_batch(Context& c, float e_b[2], float* kinetic, float mdiv[2]);
 
 // ---- sort / scan primitives --------------------------------------------------
 int key_bits_for(long long max_key_exclusive);

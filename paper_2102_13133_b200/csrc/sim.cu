@@ -541,16 +541,12 @@ struct Sim {
       out += ",total_energy,max_div_e_err,max_div_b_err,particle_count,wall_seconds_this_interval,push_rate\n";
       header_done = true;
     }
-    float eb[2];
-    field_energy(*ctx, eb);
+    float eb[2], mdiv[2];
+    std::vector<float> kin(ctx->species.size());
+    diagnostics_batch(*ctx, eb, kin.data(), mdiv);
     float total = eb[0] + eb[1];
-    launch_load_interpolators(*ctx);
-    std::vector<float> kin;
-    for (auto& s : ctx->species) {
-      kin.push_back(kinetic_energy(*ctx, s, true));
-      total += kin.back();
-    }
-    const float mde = max_abs_lane(*ctx, F_DIVE), mdb = max_abs_lane(*ctx, F_DIVB);
+    for (float k : kin) total += k;
+    const float mde = mdiv[0], mdb = mdiv[1];
     const auto now = std::chrono::steady_clock::now();
     double wall = std::chrono::duration<double>(now - last_wall).count();
     const long dsteps = step_count - last_step;
