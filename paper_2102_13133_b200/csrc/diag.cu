@@ -248,10 +248,8 @@ kinetic_kernel(const float4* __restrict__ pos, const float4* __restrict__ mom, l
       const float4 p = pos[i];
       const float4* c = interp + (size_t)__float_as_int(p.w) * kInterpF4;
       const float4 c0 = __ldg(c), c1 = __ldg(c + 1), c2 = __ldg(c + 2);
-      const float x = p.x, y = p.y, z = p.z;
-      const float ex = ((c0.x + y * c0.y) + z * c0.z) + (y * z) * c0.w;
-      const float ey = ((c1.x + z * c1.y) + x * c1.z) + (z * x) * c1.w;
-      const float ez = ((c2.x + x * c2.y) + y * c2.z) + (x * y) * c2.w;
+      float ex, ey, ez;
+      interp_eval_e(c0, c1, c2, p.x, p.y, p.z, ex, ey, ez);
       cx = cx + qdt_2m * ex;
       cy = cy + qdt_2m * ey;
       cz = cz + qdt_2m * ez;
@@ -304,10 +302,8 @@ kinetic_terms_kernel(const float4* __restrict__ pos, const float4* __restrict__ 
   const float4 p = pos[i];
   const float4* c = interp + (size_t)__float_as_int(p.w) * kInterpF4;
   const float4 c0 = __ldg(c), c1 = __ldg(c + 1), c2 = __ldg(c + 2);
-  const float x = p.x, y = p.y, z = p.z;
-  const float ex = ((c0.x + y * c0.y) + z * c0.z) + (y * z) * c0.w;
-  const float ey = ((c1.x + z * c1.y) + x * c1.z) + (z * x) * c1.w;
-  const float ez = ((c2.x + x * c2.y) + y * c2.z) + (x * y) * c2.w;
+  float ex, ey, ez;
+  interp_eval_e(c0, c1, c2, p.x, p.y, p.z, ex, ey, ez);
   const float cx = u.x + qdt_2m * ex, cy = u.y + qdt_2m * ey, cz = u.z + qdt_2m * ez;
   const float gm = __fsqrt_rn(1.0f + ((cx * cx + cy * cy) + cz * cz));
   term[i] = (u.w * m) * (gm - 1.0f);

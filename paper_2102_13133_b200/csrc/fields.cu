@@ -84,28 +84,28 @@ load_interpolators_kernel(GridC g, Lanes L, float4* __restrict__ out, float4* __
   const float* __restrict__ fey = L.p[F_EY];
   const float* __restrict__ fez = L.p[F_EZ];
   float w0, w1, w2, w3;
-  float4 r0, r1, r2, r3, r4;
+  float4 r0, r1, r2, r3, r4;  // the paired record layout (pic_device.cuh)
   w0 = fex[v]; w1 = fex[v + sy]; w2 = fex[v + sz]; w3 = fex[v + sy + sz];
-  r0.x = 0.25f * ((w3 + w0) + (w1 + w2));
-  r0.y = 0.25f * ((w3 - w0) + (w1 - w2));
-  r0.z = 0.25f * ((w3 - w0) - (w1 - w2));
-  r0.w = 0.25f * ((w3 + w0) - (w1 + w2));
+  r0.x = 0.25f * ((w3 + w0) + (w1 + w2));  // ex
+  r0.z = 0.25f * ((w3 - w0) + (w1 - w2));  // dexdy
+  r1.x = 0.25f * ((w3 - w0) - (w1 - w2));  // dexdz
+  r1.z = 0.25f * ((w3 + w0) - (w1 + w2));  // d2exdydz
   w0 = fey[v]; w1 = fey[v + sz]; w2 = fey[v + sx]; w3 = fey[v + sz + sx];
-  r1.x = 0.25f * ((w3 + w0) + (w1 + w2));
-  r1.y = 0.25f * ((w3 - w0) + (w1 - w2));
-  r1.z = 0.25f * ((w3 - w0) - (w1 - w2));
-  r1.w = 0.25f * ((w3 + w0) - (w1 + w2));
+  r0.y = 0.25f * ((w3 + w0) + (w1 + w2));  // ey
+  r0.w = 0.25f * ((w3 - w0) + (w1 - w2));  // deydz
+  r1.y = 0.25f * ((w3 - w0) - (w1 - w2));  // deydx
+  r1.w = 0.25f * ((w3 + w0) - (w1 + w2));  // d2eydzdx
   w0 = fez[v]; w1 = fez[v + sx]; w2 = fez[v + sy]; w3 = fez[v + sx + sy];
   r2.x = 0.25f * ((w3 + w0) + (w1 + w2));
   r2.y = 0.25f * ((w3 - w0) + (w1 - w2));
   r2.z = 0.25f * ((w3 - w0) - (w1 - w2));
   r2.w = 0.25f * ((w3 + w0) - (w1 + w2));
   w0 = L.p[F_BX][v]; w1 = L.p[F_BX][v + sx];
-  r3.x = 0.5f * (w1 + w0);
-  r3.y = 0.5f * (w1 - w0);
+  r3.x = 0.5f * (w1 + w0);  // cbx
+  r3.z = 0.5f * (w1 - w0);  // dcbxdx
   w0 = L.p[F_BY][v]; w1 = L.p[F_BY][v + sy];
-  r3.z = 0.5f * (w1 + w0);
-  r3.w = 0.5f * (w1 - w0);
+  r3.y = 0.5f * (w1 + w0);  // cby
+  r3.w = 0.5f * (w1 - w0);  // dcbydy
   w0 = L.p[F_BZ][v]; w1 = L.p[F_BZ][v + sz];
   r4.x = 0.5f * (w1 + w0);
   r4.y = 0.5f * (w1 - w0);
@@ -491,17 +491,17 @@ __global__ void interp_to_lanes_kernel(const float4* __restrict__ c, size_t V, f
   if (v >= V) return;
   const float4* r = c + v * kInterpF4;
   const float4 a = r[0], b = r[1], d = r[2], e = r[3], h = r[4];
-  const float vals[18] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, d.x, d.y, d.z, d.w,
-                          e.x, e.y, e.z, e.w, h.x, h.y};
+  const float slots[18] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w, d.x, d.y, d.z, d.w,
+                           e.x, e.y, e.z, e.w, h.x, h.y};
 #pragma unroll
-  for (int l = 0; l < 18; ++l) o[(size_t)l * V + v] = vals[l];
+  for (int l = 0; l < 18; ++l) o[(size_t)l * V + v] = slots[interp_slot(l)];
 }
 __global__ void lanes_to_interp_kernel(const float* __restrict__ in, size_t V, float4* __restrict__ c) {
   const size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= V) return;
   float x[20];
 #pragma unroll
-  for (int l = 0; l < 18; ++l) x[l] = in[(size_t)l * V + v];
+  for (int l = 0; l < 18; ++l) x[interp_slot(l)] = in[(size_t)l * V + v];
   x[18] = 0.f;
   x[19] = 0.f;
   float4* r = c + v * kInterpF4;

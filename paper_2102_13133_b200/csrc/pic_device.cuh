@@ -51,11 +51,30 @@ __device__ __forceinline__ unsigned fast_div(unsigned v, unsigned long long m) {
   return (unsigned)__umul64hi((unsigned long long)v, m);
 }
 
-// Interpolator record: 18 coefficients padded to 5 float4 (80 B), in the
-// reference lane order (lanes.hpp:48-69):
-//   [0] ex dexdy dexdz d2exdydz  [1] ey deydz deydx d2eydzdx
-//   [2] ez dezdx dezdy d2ezdxdy  [3] cbx dcbxdx cby dcbydy  [4] cbz dcbzdz 0 0
+// Interpolator record: the 18 coefficients of the reference's lanes
+// (lanes.hpp:48-69: ex dexdy dexdz d2exdydz, ey deydz deydx d2eydzdx,
+// ez dezdx dezdy d2ezdxdy, cbx dcbxdx, cby dcbydy, cbz dcbzdz) padded to 5
+// float4 (80 B), arranged so the push evaluates E_x, E_y and B_x, B_y as
+// register pairs (packed FP32, push.cu):
+//   [0] ex ey dexdy deydz          [1] dexdz deydx d2exdydz d2eydzdx
+//   [2] ez dezdx dezdy d2ezdxdy    [3] cbx cby dcbxdx dcbydy   [4] cbz dcbzdz 0 0
 constexpr int kInterpF4 = 5;
+// float slot of the record holding reference lane l (0..17)
+__host__ __device__ constexpr int interp_slot(int l) {
+  return l < 4 ? (l == 0 ? 0 : l == 1 ? 2 : l == 2 ? 4 : 6)
+       : l < 8 ? (l == 4 ? 1 : l == 5 ? 3 : l == 6 ? 5 : 7)
+       : l < 12 ? l
+       : l < 16 ? (l == 12 ? 12 : l == 13 ? 14 : l == 14 ? 13 : 15)
+       : l;
+}
+// E at offsets (x, y, z) in the reference's association order
+// (eval_eb_lanes, push_math.hpp:22-39)
+__device__ __forceinline__ void interp_eval_e(const float4 F0, const float4 F1, const float4 F2, float x, float y,
+                                              float z, float& ex, float& ey, float& ez) {
+  ex = ((F0.x + y * F0.z) + z * F1.x) + (y * z) * F1.z;
+  ey = ((F0.y + z * F0.w) + x * F1.y) + (z * x) * F1.w;
+  ez = ((F2.x + x * F2.y) + y * F2.z) + (x * y) * F2.w;
+}
 // Accumulator record: 12 lanes (accum_var, lanes.hpp:72-91) = 3 float4.
 constexpr int kAccF4 = 3;
 
