@@ -672,6 +672,19 @@ int pic_species_upload_records(pic_context* ctx, int species, size_t n, const vo
 int pic_species_download_records(pic_context* ctx, int species, void* pos16, void* mom16) {
   return guard([&] {
     Context& c = C_(ctx);
+    // device buffers of a voxel-ordered store: scattered into logical order
+    // directly, the store keeps its order (no regrouping after a download)
+    Species& sr = species_ref(c, species);
+    cudaPointerAttributes ap{}, am{};
+    if (cudaPointerGetAttributes(&ap, pos16) == cudaSuccess && cudaPointerGetAttributes(&am, mom16) == cudaSuccess &&
+        ap.type == cudaMemoryTypeDevice && am.type == cudaMemoryTypeDevice) {
+      settle_count(c, sr);
+      if (copy_logical(c, sr, static_cast<float4*>(pos16), static_cast<float4*>(mom16))) {
+        quiesce(c);
+        return;
+      }
+    }
+    cudaGetLastError();  // a host pointer: attributes may report an error on older drivers
     Species& s = species_at(c, species);
     quiesce(c);
     if (s.n == 0) return;

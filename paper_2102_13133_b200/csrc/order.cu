@@ -477,6 +477,20 @@ void after_ordered_push(Context& c, Species& s, bool reordered, bool counted) {
   s.counts_ready = counted;
 }
 
+// The records of a voxel-ordered species in logical order into device
+// buffers without leaving the order (the store, its chunks and logical
+// indices stay as they are): false when that is not possible (not ordered,
+// a relabel owed, a count on the device).
+bool copy_logical(Context& c, Species& s, float4* pos, float4* mom) {
+  if (!s.ordered || s.relabel_pending || s.perm_pending || s.n_on_device) return false;
+  const long long n = (long long)s.n;
+  if (n > 0) {
+    to_logical_kernel<<<blocks_of(n), 256, 0, c.stream>>>(s.lidx, n, s.pos, s.mom, pos, mom);
+    c.count_launch();
+  }
+  return true;
+}
+
 void leave_voxel_order(Context& c, Species& s) {
   if (!s.ordered) return;
   s.ordered = false;

@@ -301,6 +301,7 @@ void radix_sort_pairs(Context& c, const unsigned* keys, const unsigned* vals, si
 void sort_species(Context& c, Species& s, int order);
 // continuous voxel order (order.cu)
 bool voxel_order_usable(const Context& c);
+bool copy_logical(Context& c, Species& s, float4* pos, float4* mom);  // order.cu
 void enter_voxel_order(Context& c, Species& s);  // logical indices of the current store
 void ensure_count_buffers(Context& c, Species& s);  // vcnt / vcur / scan, pos_alt (physical order)
 void count_stored_voxels(Context& c, Species& s);   // vcnt += records per stored voxel

@@ -86,3 +86,75 @@ def test_full_scale_push_sample_bitwise_decks(name):
     finally:
         ctx.close()
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("name,sorted_first", [("weak", False), ("weak", True), ("harris", True)])
+def test_full_scale_step_sample_bitwise_decks(name, sorted_first):
+    """The step's own push at full size — every species in one launch
+    (interleaved for the two thermal species, contiguous for Harris' four),
+    in place, or reordering with the relabel of a blocked sort just before
+    it: 2^20 sampled particles per species against the oracle's push
+    through the interpolators of the step's fields (after a sort, the
+    samples are found at their stable-counting-sort positions)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    if torch.cuda.get_device_properties(0).total_memory < 150e9:
+        pytest.skip("needs a 180 GB B200")
+    from oracle.bindings import Grid as OGrid
+    from oracle.bindings import Orc
+    ctx, g, cfg, sids = _build(name)
+    try:
+        for _ in range(3):
+            ctx.step()
+        orc = Orc()
+        og = OGrid(g.nx, g.ny, g.nz, g.hx, g.hy, g.hz, g.dt)
+        f = ctx.download_fields()
+        i18 = orc.load_interpolators(og, f)
+        del f
+        rng = np.random.default_rng(13)
+        before = []
+        for sid in sids:
+            n = ctx.species_count(sid)
+            pos = torch.empty((n, 4), dtype=torch.float32, device="cuda")
+            mom = torch.empty((n, 4), dtype=torch.float32, device="cuda")
+            torch.cuda.synchronize()
+            ctx.download_records(sid, pos, mom)
+            torch.cuda.synchronize()
+            idx = torch.from_numpy(np.sort(rng.choice(n, min(n, 1 << 20), replace=False))).cuda()
+            at = idx
+            if sorted_first:  # where the blocked sort puts them: the stable argsort's inverse
+                perm = torch.sort(pos[:, 3].contiguous().view(torch.int32), stable=True).indices
+                inv = torch.empty_like(perm)
+                inv[perm] = torch.arange(n, device="cuda")
+                at = inv[idx]
+                del perm, inv
+            before.append((at, pos[idx].cpu().numpy(), mom[idx].cpu().numpy()))
+            del pos, mom
+            torch.cuda.empty_cache()
+        if sorted_first:
+            for sid in sids:  # a blocked sort: the step's push reorders and relabels
+                ctx.sort_particles(sid)
+        b0 = ctx._batched_launches()
+        ctx.step()
+        assert ctx._batched_launches() > b0
+        for sid, (sname, q, m, *_rest), (at, p0, u0) in zip(sids, cfg["species"], before):
+            n = ctx.species_count(sid)
+            pos = torch.empty((n, 4), dtype=torch.float32, device="cuda")
+            mom = torch.empty((n, 4), dtype=torch.float32, device="cuda")
+            torch.cuda.synchronize()
+            ctx.download_records(sid, pos, mom)
+            torch.cuda.synchronize()
+            p1, u1 = pos[at].cpu().numpy(), mom[at].cpu().numpy()
+            del pos, mom
+            torch.cuda.empty_cache()
+            p7 = np.ascontiguousarray(np.concatenate([p0[:, 0:3].T, u0[:, 0:4].T]), np.float32)
+            ids = np.ascontiguousarray(p0[:, 3].view(np.int32))
+            acc = np.zeros((g.padded, 12), np.float32)
+            orc.advance_particles(og, q, m, p7, ids, i18, acc)
+            got = np.concatenate([p1[:, 0:3].T, u1[:, 0:4].T])
+            assert (p1[:, 3].view(np.int32) == ids).all(), f"{name}/{sname}: voxel ids"
+            assert (got.view(np.uint32) == p7.view(np.uint32)).all(), f"{name}/{sname}: particle lanes"
+    finally:
+        ctx.close()
+        torch.cuda.empty_cache()
