@@ -640,14 +640,26 @@ int pic_species_upload(pic_context* ctx, int species, size_t n, const float* lan
 int pic_species_download(pic_context* ctx, int species, float* lanes7, int32_t* ids) {
   return guard([&] {
     Context& c = C_(ctx);
-    Species& s = species_at(c, species);
+    // a voxel-ordered store is copied out in logical order and keeps its
+    // own order (hooks and dumps do not force a regrouping)
+    Species& sr = species_ref(c, species);
+    settle_count(c, sr);
+    float4* lg = nullptr;
+    if (sr.ordered && !sr.relabel_pending && !sr.perm_pending && !sr.n_on_device && sr.n) {
+      lg = static_cast<float4*>(c.scratch_bytes(Context::kScrLogical, sr.n * 32));
+      if (!copy_logical(c, sr, lg, lg + sr.n)) lg = nullptr;
+    }
+    Species& s = lg ? sr : species_at(c, species);
     quiesce(c);
     const size_t n = s.n;
     if (n == 0) return;
     char* stg = static_cast<char*>(c.scratch_bytes(Context::kScrStaging, n * 32));
     float* d7 = reinterpret_cast<float*>(stg);
     int32_t* did = reinterpret_cast<int32_t*>(stg + n * 28);
-    launch_unpack_species(c, s, d7, did);
+    if (lg)
+      launch_unpack_records(c, lg, lg + n, n, d7, did);
+    else
+      launch_unpack_species(c, s, d7, did);
     check_launch();
     CUDA_OK(cudaMemcpyAsync(lanes7, d7, n * 28, cudaMemcpyDeviceToHost, c.stream));
     CUDA_OK(cudaMemcpyAsync(ids, did, n * 4, cudaMemcpyDeviceToHost, c.stream));

@@ -700,6 +700,11 @@ void launch_unpack_species(Context& c, Species& s, float* l7, int32_t* ids) {
   unpack_species_kernel<<<(unsigned)((s.n + 255) / 256), 256, 0, c.stream>>>(s.pos, s.mom, s.n, l7, ids);
   c.count_launch();
 }
+void launch_unpack_records(Context& c, const float4* pos, const float4* mom, size_t n, float* l7, int32_t* ids) {
+  if (n == 0) return;
+  unpack_species_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(pos, mom, n, l7, ids);
+  c.count_launch();
+}
 
 void launch_load_synthetic(Context& c, Species& s, int ppc, float u_th, const float drift[3],
                            uint64_t seed, const pic_sheet* sheet) {

@@ -151,6 +151,13 @@ def test_graphed_ordered_steps_match_oracle(pic, orc, m, prepared):
                 g0 = ctx._graph_stats()
             ctx.step()
             orc.step(o, state, wf)
+            if k == 13:  # a mid-cycle host download reads the logical order without regrouping
+                for sid, (_, _, p, ids) in zip(sids, state):
+                    assert ctx._species_ordered(sid)
+                    gp, gids = ctx.download_species(sid)
+                    assert ctx._species_ordered(sid)
+                    assert_bitwise(gids, ids, f"ids s{sid} step {k}")
+                    assert_bitwise(gp, p, f"lanes s{sid} step {k}")
             if k % 5 == 0:
                 for sid in sids:
                     ctx.sort_particles(sid)
