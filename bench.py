@@ -716,18 +716,18 @@ def run_e2e_simstate(cfg, args, steps=None, diag_interval=10):
     and SimState::run (sim.cpp:285-306: step, the due sorts, the
     diagnostics row every diag_interval steps with its charge refresh,
     written as the reference's CSV).  Timed by the wall clock around a
-    second run() (the first, a warm-up, captures the step graphs of a sort
-    cycle); per step the host reads back only the diagnostics (pic_diag +
+    second run() of five sort cycles (the first, a warm-up, captures the
+    step graphs); per step the host reads back only the diagnostics (pic_diag +
     kinetic per species, every diag_interval steps)."""
     import tempfile
 
     from paper_2102_13133_b200.simstate import Deck, SimState
-    steps = steps or cfg["sort_interval"]
+    steps = steps or 5 * cfg["sort_interval"]
     text = deck_text(cfg).replace("steps = 0", f"steps = {steps}") + f"diag_interval = {diag_interval}\n"
     sim = SimState.initialize(Deck(text), device=args.device)
     npart = sum(sim.context.species_count(k) for k in range(len(cfg["species"])))
     with tempfile.NamedTemporaryFile(suffix=".csv") as f:
-        sim.run(f.name)  # warm-up run: captures the step graphs of a sort cycle (steps = sort_interval)
+        sim.run(f.name)  # warm-up run: captures the step graphs of the sort cycles
         sim.context.synchronize()
         t0 = time.perf_counter()
         sim.run(f.name)  # steps more steps, CSV rows on the diag cadence; quiesces at the end

@@ -397,7 +397,9 @@ int pic_sim_context(pic_sim* sim, pic_context** out);
 int pic_sim_step(pic_sim* sim);
 int pic_sim_step_count(pic_sim* sim, long* out);
 int pic_sim_refresh_charge_diagnostics(pic_sim* sim);
-/* SimState::emit_diagnostics: the CSV header on first use, then one row. */
+/* SimState::emit_diagnostics: the CSV header on first use, then one row.
+ * A call with a null or short buffer computes the row, reports its length
+ * and keeps it: the next call returns that same row. */
 int pic_sim_emit_diagnostics(pic_sim* sim, char* buf, size_t cap, size_t* len);
 /* SimState::run: deck.grid.steps steps with the diagnostic / sort / dump
  * cadences; CSV to csv_path unless NULL; dumps into run.out_dir. */

@@ -428,6 +428,9 @@ struct Sim {
   unsigned flags() const {
     return (deck.deterministic ? PIC_DETERMINISTIC : 0u) | (deck.exact_gyration ? PIC_EXACT_GYRATION : 0u);
   }
+  std::string kept_row;  // pic_sim_emit_diagnostics: computed by a size query, returned by the fill
+  bool row_kept = false;
+
   size_t total_particles() const {
     size_t n = 0;
     for (const auto& s : ctx->species) n += s.n;
@@ -779,7 +782,15 @@ int pic_sim_refresh_charge_diagnostics(pic_sim* s) {
 }
 int pic_sim_emit_diagnostics(pic_sim* s, char* buf, size_t cap, size_t* len) {
   return capi_guard([&] {
-    const size_t n = copy_out(S_(s).diagnostics_row(), buf, cap);
+    // a size query (or a short buffer) computes the row and keeps it: the
+    // next call returns the same row, not a second one
+    Sim& m = S_(s);
+    if (!m.row_kept) {
+      m.kept_row = m.diagnostics_row();
+      m.row_kept = true;
+    }
+    const size_t n = copy_out(m.kept_row, buf, cap);
+    if (buf && cap > n) m.row_kept = false;
     if (len) *len = n;
   });
 }

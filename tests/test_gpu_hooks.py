@@ -98,3 +98,21 @@ def test_hook_failure_is_run_abort_and_bad_interval_usage_error():
     with _sim() as s:
         with pytest.raises(pic.UsageError, match="interval must be >= 1"):
             s.register_hook(lambda h: None, interval=0)
+
+
+def test_emit_diagnostics_returns_header_then_one_row_per_call():
+    """SimState::emit_diagnostics (sim.cpp:230-266) through the size-query /
+    fill protocol of the C-ABI: each call is one row (the header with the
+    first), with the interval's wall time measured from the previous row."""
+    sim = _sim()
+    try:
+        first = sim.emit_diagnostics().splitlines()
+        assert len(first) == 2 and first[0].startswith("step,time,e_energy,b_energy,kinetic_electron")
+        assert first[1].split(",")[0] == "0"
+        for k in range(1, 4):
+            sim.step()
+            row = sim.emit_diagnostics().splitlines()
+            assert len(row) == 1 and row[0].split(",")[0] == str(k)
+            assert float(row[0].split(",")[-1]) > 0  # push_rate over a real interval
+    finally:
+        sim.close()
