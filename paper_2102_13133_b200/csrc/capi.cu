@@ -644,20 +644,16 @@ int pic_species_download(pic_context* ctx, int species, float* lanes7, int32_t* 
     // own order (hooks and dumps do not force a regrouping)
     Species& sr = species_ref(c, species);
     settle_count(c, sr);
-    float4* lg = nullptr;
-    if (sr.ordered && !sr.relabel_pending && !sr.perm_pending && !sr.n_on_device && sr.n) {
-      lg = static_cast<float4*>(c.scratch_bytes(Context::kScrLogical, sr.n * 32));
-      if (!copy_logical(c, sr, lg, lg + sr.n)) lg = nullptr;
-    }
-    Species& s = lg ? sr : species_at(c, species);
+    const bool logical = sr.ordered && !sr.relabel_pending && !sr.perm_pending;
+    Species& s = logical ? sr : species_at(c, species);
     quiesce(c);
     const size_t n = s.n;
     if (n == 0) return;
     char* stg = static_cast<char*>(c.scratch_bytes(Context::kScrStaging, n * 32));
     float* d7 = reinterpret_cast<float*>(stg);
     int32_t* did = reinterpret_cast<int32_t*>(stg + n * 28);
-    if (lg)
-      launch_unpack_records(c, lg, lg + n, n, d7, did);
+    if (logical)
+      launch_unpack_logical(c, s, d7, did);
     else
       launch_unpack_species(c, s, d7, did);
     check_launch();

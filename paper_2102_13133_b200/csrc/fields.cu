@@ -477,14 +477,18 @@ __global__ void pack_species_kernel(const float* __restrict__ l7, const int32_t*
   pos[i] = make_float4(l7[i], l7[n + i], l7[2 * n + i], __int_as_float(ids[i]));
   mom[i] = make_float4(l7[3 * n + i], l7[4 * n + i], l7[5 * n + i], l7[6 * n + i]);
 }
+// records -> 7 lanes + ids; with lidx (a voxel-ordered store) record i
+// lands at its logical index lidx[i] (the store keeps its own order)
 __global__ void unpack_species_kernel(const float4* __restrict__ pos, const float4* __restrict__ mom,
-                                      size_t n, float* __restrict__ l7, int32_t* __restrict__ ids) {
+                                      const unsigned* __restrict__ lidx, size_t n, float* __restrict__ l7,
+                                      int32_t* __restrict__ ids) {
   const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const float4 p = pos[i], u = mom[i];
-  l7[i] = p.x; l7[n + i] = p.y; l7[2 * n + i] = p.z;
-  l7[3 * n + i] = u.x; l7[4 * n + i] = u.y; l7[5 * n + i] = u.z; l7[6 * n + i] = u.w;
-  ids[i] = __float_as_int(p.w);
+  const size_t d = lidx ? (size_t)lidx[i] : i;
+  l7[d] = p.x; l7[n + d] = p.y; l7[2 * n + d] = p.z;
+  l7[3 * n + d] = u.x; l7[4 * n + d] = u.y; l7[5 * n + d] = u.z; l7[6 * n + d] = u.w;
+  ids[d] = __float_as_int(p.w);
 }
 __global__ void interp_to_lanes_kernel(const float4* __restrict__ c, size_t V, float* __restrict__ o) {
   const size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -697,12 +701,13 @@ void launch_pack_species(Context& c, Species& s, const float* l7, const int32_t*
 
 void launch_unpack_species(Context& c, Species& s, float* l7, int32_t* ids) {
   if (s.n == 0) return;
-  unpack_species_kernel<<<(unsigned)((s.n + 255) / 256), 256, 0, c.stream>>>(s.pos, s.mom, s.n, l7, ids);
+  unpack_species_kernel<<<(unsigned)((s.n + 255) / 256), 256, 0, c.stream>>>(s.pos, s.mom, nullptr, s.n, l7,
+                                                                              ids);
   c.count_launch();
 }
-void launch_unpack_records(Context& c, const float4* pos, const float4* mom, size_t n, float* l7, int32_t* ids) {
-  if (n == 0) return;
-  unpack_species_kernel<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(pos, mom, n, l7, ids);
+void launch_unpack_logical(Context& c, const Species& s, float* l7, int32_t* ids) {
+  if (s.n == 0) return;
+  unpack_species_kernel<<<(unsigned)((s.n + 255) / 256), 256, 0, c.stream>>>(s.pos, s.mom, s.lidx, s.n, l7, ids);
   c.count_launch();
 }
 

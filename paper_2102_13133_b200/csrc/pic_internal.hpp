@@ -167,7 +167,7 @@ struct Context {
     kScrStage = 0, kScrNseg, kScrOff, kScrSegKey, kScrSegW,
     kScrKeyA, kScrValA, kScrKeyB, kScrValB, kScrHist, kScrScan,
     kScrCount, kScrStart, kScrWithin, kScrStaging, kScrSmall, kScrDiag, kScrMigA, kScrMigB, kScrMigC, kScrMigT,
-    kScrWall, kScrDiagLines, kScrLogical, kScrN
+    kScrWall, kScrDiagLines, kScrN
   };
   void* scratch[kScrN] = {};
   size_t scratch_size[kScrN] = {};
@@ -242,7 +242,8 @@ void launch_clear_accumulator(Context& c);
 void launch_pack_species(Context& c, Species& s, const float* lanes7_dev, const int32_t* ids_dev,
                          size_t n);
 void launch_unpack_species(Context& c, Species& s, float* lanes7_dev, int32_t* ids_dev);
-void launch_unpack_records(Context& c, const float4* pos, const float4* mom, size_t n, float* l7, int32_t* ids);
+// a voxel-ordered store (no relabel / permutation pending) to lanes in logical order
+void launch_unpack_logical(Context& c, const Species& s, float* l7, int32_t* ids);
 void launch_load_synthetic(Context& c, Species& s, int ppc, float u_th, const float drift[3],
                            uint64_t seed, const pic_sheet* sheet);
 void launch_interp_to_lanes(Context& c, float* out18);
