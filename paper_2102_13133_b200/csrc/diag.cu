@@ -143,16 +143,21 @@ div_errors_kernel(GridC g, float* __restrict__ f, float rhx, float rhy, float rh
 // deposit_rho (particles.cpp:384-410): eight trilinear weights per particle
 // into the rhof lane (float atomics, order not fixed: tolerance parity).
 // A CTA takes 2048 consecutive records; each lane sums runs of equal voxels
-// over consecutive records of its own (4 per round, staged through shared
-// memory from coalesced loads, two rounds), so a voxel-ordered store adds
-// once per node per lane and run, with fire-and-forget reductions in L2.
+// over 8 consecutive records of its own (staged through shared memory from
+// coalesced loads), so a voxel-ordered store adds once per node per lane
+// and run, with fire-and-forget reductions in L2.
 // Measured at C1 (8.4 M records, ncu): 132 us for the previous form (a
 // segmented shuffle scan of one record per lane, then shared-memory windows
 // whose float atomics compile to a CAS loop: issue-bound), 98 us with the
-// lane runs and scalar REDs, 108 us with red.v2 for the x-adjacent node
-// pairs when 8-B aligned.
-constexpr int kRhoLane = 4;    // consecutive records per lane and round
-constexpr int kRhoRounds = 2;  // rounds per CTA: 256 * 4 * 2 = 2048 records
+// lane runs of 4 and scalar REDs, 108 us with red.v2 for the x-adjacent
+// node pairs when 8-B aligned; refresh_charge at C1 (two species + div
+// errors) 0.205 ms with runs of 4 per lane, 0.157 ms with 8, 0.39 with 2.
+#ifndef PIC_RHO_LANE
+#define PIC_RHO_LANE 8
+#define PIC_RHO_ROUNDS 1
+#endif
+constexpr int kRhoLane = PIC_RHO_LANE;      // consecutive records per lane and round
+constexpr int kRhoRounds = PIC_RHO_ROUNDS;  // rounds per CTA: 256 * 8 = 2048 records
 __device__ __forceinline__ void rho_flush(const GridC& g, int key, const float* w, float* __restrict__ rho) {
   const unsigned rest = fast_div((unsigned)key, g.mag_pnx);
   const int ix = key - (int)rest * g.pnx;
